@@ -1,0 +1,152 @@
+"""Pin the CPU oracle against outputs of the real reference (tests/golden/).
+
+The fixtures were produced by `tests/golden/make_golden.py` running the
+unmodified reference; these checks make the oracle a trustworthy checker for
+the CUDA path (CPU only)."""
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from oracle import nedf_oracle as O
+from paper_2308_04669_b200 import configs as C
+from tests.conftest import GOLDEN
+from tests.helpers import oracle_model, oracle_scene
+
+
+def test_clip_and_encoding(golden):
+    z = golden("geometry.npz")
+    t0, t1, hit = O.slab_clip(z["origins"], z["dirs"], z["box_min"], z["box_max"])
+    np.testing.assert_array_equal(hit, z["hit"])
+    np.testing.assert_array_equal(t0[hit], z["t0"][hit])
+    np.testing.assert_array_equal(t1[hit], z["t1"][hit])
+    feats, h2 = O.encode_rays(z["origins"], z["dirs"], z["box_min"], z["box_max"])
+    np.testing.assert_array_equal(h2, z["hit"])
+    np.testing.assert_allclose(feats[z["enc_rows"]], z["enc"], rtol=0, atol=1e-12)
+
+
+def test_primary_rays(golden):
+    z = golden("geometry.npz")
+    cam = O.Cam(np.array([1.0, 2.0, 3.0]), O.look_at([1, 2, 3], [0, 0, 0]), 0.8, 7, 5)
+    o, d = O.primary_rays(cam)
+    np.testing.assert_allclose(d, z["cam_dirs"], atol=1e-15)
+    np.testing.assert_array_equal(o, z["cam_origins"])
+    # pixel subsets are exact
+    sub = np.array([0, 5, 34])
+    o2, d2 = O.primary_rays(cam, sub)
+    np.testing.assert_array_equal(d2, d[sub])
+
+
+@pytest.mark.parametrize("key", json.loads((GOLDEN / "models.json").read_text()).keys())
+def test_random_init_matches_reference_bytes(key):
+    ref = json.loads((GOLDEN / "models.json").read_text())[key]
+    seed, kind = key.split(":")
+    m = oracle_model(int(seed), kind)
+    raw = O.nedm_bytes(m)
+    assert len(raw) == ref["bytes"]
+    assert hashlib.sha256(raw).hexdigest() == ref["sha256"]
+    assert m.half_range == ref["half_range"]
+    np.testing.assert_array_equal(m.box_min, ref["box_min"])
+
+
+@pytest.mark.parametrize("name", ["0_sphere", "1_box", "5_torus", "2_sphere"])
+def test_forward_and_queries(golden, name):
+    z = golden(f"forward_{name}.npz")
+    seed, kind = name.split("_")
+    m = oracle_model(int(seed), kind)
+    mu, alpha, hit, logits = O.query_local(m, z["origins"], z["dirs"], return_logits=True)
+    np.testing.assert_array_equal(hit, z["hit"])
+    lc, lf, la = logits
+    scale = np.abs(z["logits_c"]).max()
+    np.testing.assert_allclose(lc, z["logits_c"], rtol=0, atol=1e-9 * scale)
+    np.testing.assert_allclose(lf, z["logits_f"], rtol=0, atol=1e-9 * scale)
+    np.testing.assert_allclose(la, z["logit_a"], rtol=0, atol=1e-9 * scale)
+    np.testing.assert_array_equal(np.isnan(mu), np.isnan(z["mu"]))
+    np.testing.assert_array_equal(mu[hit], z["mu"][hit])
+    np.testing.assert_array_equal(alpha, z["alpha"])
+    depth, walpha = O.world_depth(m, z["R"], z["T"], float(z["s"]), z["world_o"], z["world_d"])
+    np.testing.assert_array_equal(walpha, z["world_alpha"])
+    ok = np.isfinite(z["world_depth"])
+    np.testing.assert_allclose(depth[ok], z["world_depth"][ok], rtol=1e-12, atol=1e-12)
+
+
+def _check_frame(out, z, shadows=True):
+    np.testing.assert_array_equal(out.id, z["id"])
+    fin = np.isfinite(z["depth"])
+    np.testing.assert_array_equal(np.isfinite(out.depth), fin)
+    np.testing.assert_allclose(out.depth[fin], z["depth"][fin], rtol=1e-12, atol=1e-12)
+    if "rgb" in z:
+        np.testing.assert_allclose(out.rgb, z["rgb"], atol=1e-12)
+        np.testing.assert_array_equal(out.shadow, z["shadow"])
+        np.testing.assert_allclose(out.image, z["image"], atol=1e-12)
+
+
+def test_frame_config1(golden):
+    objs, cam, lights, cfg = oracle_scene(C.config1())
+    out = O.render(objs, cam, [], cfg, threads=4)
+    _check_frame(out, golden("frame_config1.npz"))
+
+
+@pytest.mark.parametrize("fname,spec", [("frame_config4_200x80.npz", C.config4(200, 80)),
+                                        ("frame_config3_160x64.npz", C.config3(160, 64))])
+def test_frame_small_configs(golden, fname, spec):
+    z = golden(fname)
+    objs, cam, lights, cfg = oracle_scene(spec)
+    out = O.render(objs, cam, lights, cfg, threads=4)
+    _check_frame(out, z)
+    for k, ob in enumerate(objs):
+        np.testing.assert_allclose(out.planes[ob.id], z["planes"][k], rtol=1e-12, atol=1e-12)
+
+
+def test_frame_pixel_subset_is_exact(golden):
+    z = golden("frame_config4_200x80.npz")
+    objs, cam, lights, cfg = oracle_scene(C.config4(200, 80))
+    pix = np.random.default_rng(0).choice(200 * 80, size=500, replace=False)
+    out = O.render(objs, cam, lights, cfg, pixels=pix, threads=4)
+    np.testing.assert_array_equal(out.id, z["id"].ravel()[pix])
+    np.testing.assert_allclose(out.image, z["image"].reshape(-1, 3)[pix], atol=1e-12)
+
+
+def test_frame_two_lights(golden):
+    spec = C.config4(96, 40)
+    spec.objects = spec.objects[:4]
+    spec.lights = [C.LightSpec("point", (0.0, 6.0, -2.0), 0.4),
+                   C.LightSpec("directional", (0.0, -1.0, 0.0), 0.3)]
+    objs, cam, lights, cfg = oracle_scene(spec)
+    out = O.render(objs, cam, lights, cfg, threads=4)
+    _check_frame(out, golden("frame_twolights_96x40.npz"))
+
+
+def test_analytic_backend_frame(golden):
+    z = golden("frame_analytic_48.npz")
+    slab = ("box", (0.0, 0.0, 0.0), (4.0, 0.5, 4.0))
+    sph = ("sphere", (0.0, 0.0, 0.0), 0.5)
+    objs = [O.Obj(0, np.eye(3), np.array([0, -0.5, 0.0]), 1.0, slab),
+            O.Obj(1, np.eye(3), np.array([0, 2.5, 0.0]), 1.0, sph)]
+    cam = O.Cam(np.array([0, 2.5, 5.5]), O.look_at([0, 2.5, 5.5], [0, 0.5, 0]), 1.1, 48, 48)
+    out = O.render(objs, cam, [O.Light("point", np.array([0, 5.0, 0]), 0.4)])
+    _check_frame(out, z)
+    out2 = O.render(objs, cam, [O.Light("directional", np.array([0, -1.0, 0]), 0.3)])
+    np.testing.assert_array_equal(out2.shadow, z["shadow_dir"])
+    np.testing.assert_allclose(out2.image, z["image_dir"], atol=1e-12)
+
+
+def test_voxel_sample(golden):
+    z = golden("voxel_probe.npz")
+    prim = ("voxel", z["density"].shape, z["bmin"], z["bmax"], z["density"], z["color"])
+    rgb, sig = O.voxel_sample(prim, z["points"])
+    np.testing.assert_allclose(rgb, z["rgb"], atol=1e-14)
+    np.testing.assert_allclose(sig, z["sigma"], atol=1e-14)
+
+
+def test_nedm_format_errors():
+    m = oracle_model(0, "sphere")
+    raw = O.nedm_bytes(m)
+    with pytest.raises(ValueError):
+        O.parse_nedm(b"XXXX" + raw[4:])
+    with pytest.raises(ValueError):
+        O.parse_nedm(raw[:-1])
+    with pytest.raises(ValueError):
+        O.parse_nedm(raw[:20])
