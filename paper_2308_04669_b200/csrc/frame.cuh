@@ -1,0 +1,63 @@
+// Host-visible declarations of the frame kernels and the network launchers.
+#pragma once
+
+#include "common.cuh"
+
+namespace nedf {
+
+struct FrameJob {
+  RayJob ray;                    // camera / light / object tables
+  const NedfField* fields;       // device copy of the field nodes
+  int n_objs;
+  int n_pix;
+  unsigned long long* key;       // per-pixel packed z-key (STEP 1 or STEP 3)
+  double* depth;                 // per-pixel depth
+  int* id;                       // per-pixel user id
+  float* rgb;
+  float* shadow;
+  float* image;
+  double* planes;                // optional [n_objs][n_pix]
+  double eps;                    // shadow epsilon
+  double beta;
+  double sigma_threshold;        // < 0: per-field default
+  int resample, resample_samples;
+  double clear[3];
+  unsigned long long* stats;     // [0] covered, [1] outliers
+};
+
+cudaError_t launch_setup(const FrameJob& fj, const GroupTable& gt, const ListSet& ls, int mode, int n_sms,
+                         cudaStream_t st);
+cudaError_t launch_step1_resolve(const FrameJob& fj, const GroupTable& gt, int n_sms, cudaStream_t st);
+cudaError_t launch_shade(const FrameJob& fj, const GroupTable& gt, int n_sms, cudaStream_t st);
+cudaError_t launch_shadow_resolve(const FrameJob& fj, const GroupTable& gt, int mode, int n_sms, cudaStream_t st);
+cudaError_t launch_fill(float* buf, int64_t n, float v, int n_sms, cudaStream_t st);
+cudaError_t launch_composite(const float* rgb, const float* shadow, float* image, int64_t n, int n_sms,
+                             cudaStream_t st);
+cudaError_t launch_explicit_setup(const RayJob& job, const GroupTable& gt, const ListSet& ls, const OutSpec& out,
+                                  int64_t n, int n_sms, cudaStream_t st);
+cudaError_t launch_iota_setup(const ListSet& ls, int64_t n, int n_sms, cudaStream_t st);
+
+// network
+size_t simt_smem_bytes();
+cudaError_t launch_mlp_fp32(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
+                            int n_sms, cudaStream_t stream);
+
+// tensor-core network (mlp_tc.cu): evaluates `ls`; with guard > 0, rays whose
+// top-2 margins fall below guard * max|logit| are appended to `redo` instead
+// of being written.
+struct TcArgs {
+  GroupTable gt;
+  ListSet ls;
+  ListSet redo;
+  RayJob job;
+  OutSpec out;
+  float guard;
+  int use_guard;
+  int* tile_counter;
+};
+bool tc_available();
+cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, cudaStream_t stream);
+cudaError_t tc_pack_weights(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
+                            __half** wpack_dev, float** bias_dev, size_t* bytes);
+
+}  // namespace nedf
