@@ -61,7 +61,8 @@ enum {
 enum {
   NEDF_OPT_PRECISION = 1,       /* one of NEDF_PREC_* */
   NEDF_OPT_GUARD_PPM = 2,       /* near-tie guard threshold tau, parts per million of max|logit| */
-  NEDF_OPT_TC_CTAS = 3          /* persistent CTAs for the tensor-core kernel (0 = one per SM) */
+  NEDF_OPT_TC_CTAS = 3,         /* persistent CTAs for the tensor-core kernel (0 = one per SM) */
+  NEDF_OPT_PROFILE = 4          /* 1 = time every network launch with CUDA events (read back by nedf_read_stats) */
 };
 
 typedef struct NedfContext NedfContext; /* one per device: streams' scratch, counters */
@@ -160,6 +161,11 @@ typedef struct {
   int64_t guarded;          /* rays re-evaluated in fp32 by the near-tie guard */
   int64_t covered;          /* pixels with id >= 0 (Step 2) */
   int64_t resampled;        /* outlier pixels (Step 2) */
+  int64_t launches;         /* kernels this library launched since the last read */
+  int64_t net_launches;     /* network-kernel launches timed (NEDF_OPT_PROFILE) */
+  double net_ms;            /* summed device time of the main network kernel (tensor-core or fp32) */
+  double guard_ms;          /* summed device time of the fp32 re-evaluation of guarded rays */
+  int64_t h2d_bytes;        /* host->device bytes this library copied (per-call scene tables) */
 } NedfStepStats;
 
 /* ---- library / context ---------------------------------------------------- */

@@ -24,7 +24,7 @@ NEDF_ERR_UNSUPPORTED = -4
 NEDF_ERR_NOMEM = -5
 
 PREC_AUTO, PREC_TENSOR, PREC_FP32 = 0, 1, 2
-OPT_PRECISION, OPT_GUARD_PPM, OPT_TC_CTAS = 1, 2, 3
+OPT_PRECISION, OPT_GUARD_PPM, OPT_TC_CTAS, OPT_PROFILE = 1, 2, 3, 4
 
 FIELD_SPHERE, FIELD_BOX, FIELD_TORUS, FIELD_PLANE, FIELD_UNION, FIELD_TRANSFORMED, FIELD_VOXEL = range(1, 8)
 DEPTH_NEDF, DEPTH_ANALYTIC = 0, 1
@@ -69,7 +69,9 @@ class NedfFrameBuffers(C.Structure):
 
 
 class NedfStepStats(C.Structure):
-    _fields_ = [("evals", C.c_int64), ("guarded", C.c_int64), ("covered", C.c_int64), ("resampled", C.c_int64)]
+    _fields_ = [("evals", C.c_int64), ("guarded", C.c_int64), ("covered", C.c_int64), ("resampled", C.c_int64),
+                ("launches", C.c_int64), ("net_launches", C.c_int64), ("net_ms", C.c_double),
+                ("guard_ms", C.c_double), ("h2d_bytes", C.c_int64)]
 
 
 P = C.c_void_p
@@ -166,7 +168,9 @@ class Context:
     def read_stats(self, stream) -> dict:
         s = NedfStepStats()
         check(self._lib.nedf_read_stats(self.handle, C.byref(s), stream))
-        return {"evals": s.evals, "guarded": s.guarded, "covered": s.covered, "resampled": s.resampled}
+        return {"evals": s.evals, "guarded": s.guarded, "covered": s.covered, "resampled": s.resampled,
+                "launches": s.launches, "net_launches": s.net_launches, "net_ms": s.net_ms,
+                "guard_ms": s.guard_ms, "h2d_bytes": s.h2d_bytes}
 
     def __del__(self):
         try:

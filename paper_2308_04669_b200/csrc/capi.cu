@@ -65,11 +65,24 @@ struct NedfContext {
   int precision = NEDF_PREC_AUTO;
   int guard_ppm = 3000;
   int tc_ctas = 0;
+  int profile = 0;
+  int64_t launches = 0;
+  // event pairs around network launches (NEDF_OPT_PROFILE); kind 0 = main, 1 = guard
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_pairs;   // (start index, kind)
+  size_t ev_used = 0;
   DevBuf models, objs, fields, rows, offsets, counts, redo_counts, lists_pix, lists_obj, redo_pix, redo_obj,
       key, skey, stats, tile_counter;
+  int64_t h2d_bytes = 0;
 };
 
 namespace {
+
+// host -> device copy of per-call tables, counted for the e2e byte report
+cudaError_t h2d_async(NedfContext* ctx, void* dst, const void* src, size_t n, cudaStream_t st) {
+  ctx->h2d_bytes += (int64_t)n;
+  return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st);
+}
 
 const int64_t kNoStats = -1;
 
@@ -153,12 +166,12 @@ int build_scene(NedfContext* ctx, const NedfObject* objs, int n_objs, const Nedf
   std::vector<DevModel> gm(std::max<size_t>(sc.group_models.size(), 1));
   for (size_t g = 0; g < sc.group_models.size(); ++g) gm[g] = sc.group_models[g]->host;
   CUDA_TRY(ctx->models.ensure(gm.size() * sizeof(DevModel)));
-  CUDA_TRY(cudaMemcpyAsync(ctx->models.ptr, gm.data(), gm.size() * sizeof(DevModel), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h2d_async(ctx, ctx->models.ptr, gm.data(), gm.size() * sizeof(DevModel), st));
   CUDA_TRY(ctx->objs.ensure(sc.objs.size() * sizeof(DevObj)));
-  CUDA_TRY(cudaMemcpyAsync(ctx->objs.ptr, sc.objs.data(), sc.objs.size() * sizeof(DevObj), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h2d_async(ctx, ctx->objs.ptr, sc.objs.data(), sc.objs.size() * sizeof(DevObj), st));
   if (n_fields > 0) {
     CUDA_TRY(ctx->fields.ensure(n_fields * sizeof(NedfField)));
-    CUDA_TRY(cudaMemcpyAsync(ctx->fields.ptr, fields, n_fields * sizeof(NedfField), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h2d_async(ctx, ctx->fields.ptr, fields, n_fields * sizeof(NedfField), st));
   }
   return NEDF_OK;
 }
@@ -249,7 +262,7 @@ int prepare_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject* obj
     for (int a = 0; a < 3; ++a) { F.sc.objs[s].rbox_min[a] = lo[a]; F.sc.objs[s].rbox_max[a] = hi[a]; }
   }
   if (n_objs > 0)
-    CUDA_TRY(cudaMemcpyAsync(ctx->objs.ptr, F.sc.objs.data(), n_objs * sizeof(DevObj), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h2d_async(ctx, ctx->objs.ptr, F.sc.objs.data(), n_objs * sizeof(DevObj), st));
   // rows
   std::vector<int> rows;
   if (fb->rows_host) {
@@ -265,14 +278,14 @@ int prepare_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject* obj
   F.n_pix = (int64_t)n_rows * cam->width;
   if (F.n_pix > 0xFFFFFFFFll) return fail(NEDF_ERR_INVALID, "frame too large");
   CUDA_TRY(ctx->rows.ensure(std::max<size_t>(rows.size(), 1) * sizeof(int)));
-  if (n_rows) CUDA_TRY(cudaMemcpyAsync(ctx->rows.ptr, rows.data(), rows.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  if (n_rows) CUDA_TRY(h2d_async(ctx, ctx->rows.ptr, rows.data(), rows.size() * sizeof(int), st));
   // lists: per group capacity = n_pix * objects of that group
   int ng = (int)F.sc.group_models.size();
   std::vector<int64_t> off(std::max(ng, 1), 0);
   int64_t cap = 0;
   for (int g = 0; g < ng; ++g) { off[g] = cap; cap += F.n_pix * F.sc.objs_per_group[g]; }
   CUDA_TRY(ctx->offsets.ensure(off.size() * sizeof(int64_t)));
-  CUDA_TRY(cudaMemcpyAsync(ctx->offsets.ptr, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h2d_async(ctx, ctx->offsets.ptr, off.data(), off.size() * sizeof(int64_t), st));
   CUDA_TRY(ctx->counts.ensure(64 * sizeof(int)));
   CUDA_TRY(ctx->redo_counts.ensure(64 * sizeof(int)));
   CUDA_TRY(ctx->lists_pix.ensure(std::max<int64_t>(cap, 1) * sizeof(uint32_t)));
@@ -326,10 +339,31 @@ __global__ void add_counts_kernel(const int* counts, const int* redo, int ng, un
   }
 }
 
+// CUDA-event bracket around a network launch when profiling is on.
+int prof_mark(NedfContext* ctx, cudaStream_t st, int kind, bool start) {
+  if (!ctx->profile) return NEDF_OK;
+  if (ctx->ev_used + 1 > ctx->ev_pool.size()) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    ctx->ev_pool.push_back(e);
+  }
+  int idx = (int)ctx->ev_used++;
+  if (start) ctx->ev_pairs.push_back({idx, kind});
+  CUDA_TRY(cudaEventRecord(ctx->ev_pool[idx], st));
+  return NEDF_OK;
+}
+
+#define LAUNCH(ctx, expr)       \
+  do {                          \
+    CUDA_TRY(expr);             \
+    (ctx)->launches += 1;       \
+  } while (0)
+
 // Evaluate the network on every list entry with the context's precision.
 int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& out, cudaStream_t st) {
   if (F.gt.n_groups == 0) return NEDF_OK;
   bool use_tc = ctx->precision != NEDF_PREC_FP32 && F.sc.all_tc && tc_available();
+  int rc;
   if (use_tc) {
     TcArgs a;
     a.gt = F.gt; a.ls = F.ls; a.redo = F.redo; a.job = job; a.out = out;
@@ -339,12 +373,22 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
     CUDA_TRY(cudaMemsetAsync(F.redo.count, 0, 64 * sizeof(int), st));
     CUDA_TRY(cudaMemsetAsync(a.tile_counter, 0, 64 * sizeof(int), st));
     int ctas = ctx->tc_ctas > 0 ? ctx->tc_ctas : ctx->n_sms;
-    CUDA_TRY(launch_mlp_tc(a, ctas, st));
-    if (a.use_guard) CUDA_TRY(launch_mlp_fp32(F.gt, F.redo, job, out, ctx->n_sms, st));
+    if ((rc = prof_mark(ctx, st, 0, true))) return rc;
+    LAUNCH(ctx, launch_mlp_tc(a, ctas, st));
+    if ((rc = prof_mark(ctx, st, 0, false))) return rc;
+    if (a.use_guard) {
+      if ((rc = prof_mark(ctx, st, 1, true))) return rc;
+      LAUNCH(ctx, launch_mlp_fp32(F.gt, F.redo, job, out, ctx->n_sms, st));
+      if ((rc = prof_mark(ctx, st, 1, false))) return rc;
+    }
     add_counts_kernel<<<1, 32, 0, st>>>(F.ls.count, F.redo.count, F.gt.n_groups, F.fj.stats, a.use_guard);
+    ctx->launches += 1;
   } else {
-    CUDA_TRY(launch_mlp_fp32(F.gt, F.ls, job, out, ctx->n_sms, st));
+    if ((rc = prof_mark(ctx, st, 0, true))) return rc;
+    LAUNCH(ctx, launch_mlp_fp32(F.gt, F.ls, job, out, ctx->n_sms, st));
+    if ((rc = prof_mark(ctx, st, 0, false))) return rc;
     add_counts_kernel<<<1, 32, 0, st>>>(F.ls.count, F.redo.count, F.gt.n_groups, F.fj.stats, 0);
+    ctx->launches += 1;
   }
   CUDA_TRY(cudaGetLastError());
   return NEDF_OK;
@@ -355,7 +399,7 @@ int do_step1(NedfContext* ctx, Frame& F, cudaStream_t st) {
   fj.ray.mode = RAY_PRIMARY;
   CUDA_TRY(cudaMemsetAsync(F.ls.count, 0, 64 * sizeof(int), st));
   if (F.n_pix == 0) return NEDF_OK;
-  CUDA_TRY(launch_setup(fj, F.gt, F.ls, RAY_PRIMARY, ctx->n_sms, st));
+  LAUNCH(ctx, launch_setup(fj, F.gt, F.ls, RAY_PRIMARY, ctx->n_sms, st));
   OutSpec out;
   memset(&out, 0, sizeof(out));
   out.mode = OUT_ZBUF;
@@ -364,7 +408,7 @@ int do_step1(NedfContext* ctx, Frame& F, cudaStream_t st) {
   out.plane_stride = F.n_pix;
   int rc = run_network(ctx, F, fj.ray, out, st);
   if (rc) return rc;
-  CUDA_TRY(launch_step1_resolve(fj, F.gt, ctx->n_sms, st));
+  LAUNCH(ctx, launch_step1_resolve(fj, F.gt, ctx->n_sms, st));
   return NEDF_OK;
 }
 
@@ -386,7 +430,7 @@ int do_step2(NedfContext* ctx, Frame& F, const NedfRenderConfig* cfg, cudaStream
   fill_config(F.fj, cfg);
   F.fj.ray.mode = RAY_PRIMARY;
   if (F.n_pix == 0) return NEDF_OK;
-  CUDA_TRY(launch_shade(F.fj, F.gt, ctx->n_sms, st));
+  LAUNCH(ctx, launch_shade(F.fj, F.gt, ctx->n_sms, st));
   return NEDF_OK;
 }
 
@@ -424,14 +468,14 @@ int do_step3(NedfContext* ctx, Frame& F, const NedfObject* objs, const NedfLight
   FrameJob sj = fj;
   sj.planes = nullptr;
   sj.key = ctx->skey.as<unsigned long long>();
-  CUDA_TRY(launch_setup(sj, F.gt, F.ls, mode, ctx->n_sms, st));
+  LAUNCH(ctx, launch_setup(sj, F.gt, F.ls, mode, ctx->n_sms, st));
   OutSpec out;
   memset(&out, 0, sizeof(out));
   out.mode = OUT_ZBUF;
   out.key = sj.key;
   int rc = run_network(ctx, F, sj.ray, out, st);
   if (rc) return rc;
-  CUDA_TRY(launch_shadow_resolve(sj, F.gt, mode, ctx->n_sms, st));
+  LAUNCH(ctx, launch_shadow_resolve(sj, F.gt, mode, ctx->n_sms, st));
   return NEDF_OK;
 }
 
@@ -487,6 +531,9 @@ int nedf_set_option(NedfContext* c, int key, int64_t v) {
       if (v < 0) return fail(NEDF_ERR_INVALID, "bad CTA count");
       c->tc_ctas = (int)v;
       return NEDF_OK;
+    case NEDF_OPT_PROFILE:
+      c->profile = v != 0;
+      return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }
@@ -497,6 +544,7 @@ int nedf_get_option(NedfContext* c, int key, int64_t* v) {
     case NEDF_OPT_PRECISION: *v = c->precision; return NEDF_OK;
     case NEDF_OPT_GUARD_PPM: *v = c->guard_ppm; return NEDF_OK;
     case NEDF_OPT_TC_CTAS: *v = c->tc_ctas; return NEDF_OK;
+    case NEDF_OPT_PROFILE: *v = c->profile; return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }
@@ -514,6 +562,24 @@ int nedf_read_stats(NedfContext* c, NedfStepStats* out, void* stream) {
   out->resampled = (int64_t)h[1];
   out->evals = (int64_t)h[2];
   out->guarded = (int64_t)h[3];
+  out->launches = c->launches;
+  c->launches = 0;
+  out->h2d_bytes = c->h2d_bytes;
+  c->h2d_bytes = 0;
+  out->net_launches = 0;
+  out->net_ms = 0.0;
+  out->guard_ms = 0.0;
+  if (!c->ev_pairs.empty()) {
+    CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    for (auto& pr : c->ev_pairs) {
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_pool[pr.first], c->ev_pool[pr.first + 1]));
+      if (pr.second == 0) { out->net_ms += ms; out->net_launches += 1; }
+      else out->guard_ms += ms;
+    }
+  }
+  c->ev_pairs.clear();
+  c->ev_used = 0;
   return NEDF_OK;
 }
 
@@ -652,10 +718,10 @@ static int single_model_frame(NedfContext* ctx, const NedfModel* m, int64_t n, F
   F.sc.all_tc = m->host.tensor_ok != 0;
   F.sc.n_objs = 1;
   CUDA_TRY(ctx->models.ensure(sizeof(DevModel)));
-  CUDA_TRY(cudaMemcpyAsync(ctx->models.ptr, &m->host, sizeof(DevModel), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h2d_async(ctx, ctx->models.ptr, &m->host, sizeof(DevModel), st));
   int64_t off0 = 0;
   CUDA_TRY(ctx->offsets.ensure(sizeof(int64_t)));
-  CUDA_TRY(cudaMemcpyAsync(ctx->offsets.ptr, &off0, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h2d_async(ctx, ctx->offsets.ptr, &off0, sizeof(int64_t), st));
   CUDA_TRY(ctx->counts.ensure(64 * sizeof(int)));
   CUDA_TRY(ctx->redo_counts.ensure(64 * sizeof(int)));
   CUDA_TRY(ctx->lists_pix.ensure(std::max<int64_t>(n, 1) * 4));
@@ -691,7 +757,7 @@ int nedf_mlp_forward(NedfContext* ctx, const NedfModel* m, const float* feats, i
   int rc = single_model_frame(ctx, m, batch, F, st);
   if (rc) return rc;
   if (batch == 0) return NEDF_OK;
-  CUDA_TRY(launch_iota_setup(F.ls, batch, ctx->n_sms, st));
+  LAUNCH(ctx, launch_iota_setup(F.ls, batch, ctx->n_sms, st));
   OutSpec out;
   memset(&out, 0, sizeof(out));
   out.mode = OUT_LOGITS;
@@ -726,7 +792,7 @@ static int query_common(NedfContext* ctx, const NedfModel* m, int mode, const do
     ob.s = 1.0;
   }
   CUDA_TRY(ctx->objs.ensure(sizeof(DevObj)));
-  CUDA_TRY(cudaMemcpyAsync(ctx->objs.ptr, &ob, sizeof(DevObj), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h2d_async(ctx, ctx->objs.ptr, &ob, sizeof(DevObj), st));
   if (n == 0) return NEDF_OK;
   RayJob job;
   memset(&job, 0, sizeof(job));
@@ -739,7 +805,7 @@ static int query_common(NedfContext* ctx, const NedfModel* m, int mode, const do
   out.mode = mode == RAY_WORLD ? OUT_QUERY_WORLD : OUT_QUERY_LOCAL;
   if (mode == RAY_WORLD) out.depth = depth_or_mu; else out.mu = depth_or_mu;
   out.alpha = alpha;
-  CUDA_TRY(launch_explicit_setup(job, F.gt, F.ls, out, n, ctx->n_sms, st));
+  LAUNCH(ctx, launch_explicit_setup(job, F.gt, F.ls, out, n, ctx->n_sms, st));
   return run_network(ctx, F, job, out, st);
 }
 
@@ -790,7 +856,7 @@ int nedf_composite(NedfContext* ctx, NedfFrameBuffers* fb, int width, void* stre
   if (!ctx || !fb) return fail(NEDF_ERR_INVALID, "NULL argument");
   int64_t n = (int64_t)fb->n_rows * width;
   if (n <= 0 || !fb->image_dev) return NEDF_OK;
-  CUDA_TRY(launch_composite(fb->rgb_dev, fb->shadow_dev, fb->image_dev, n, ctx->n_sms, (cudaStream_t)stream));
+  LAUNCH(ctx, launch_composite(fb->rgb_dev, fb->shadow_dev, fb->image_dev, n, ctx->n_sms, (cudaStream_t)stream));
   return NEDF_OK;
 }
 
@@ -806,7 +872,7 @@ int nedf_render_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject*
   if (rc) return rc;
   rc = do_step2(ctx, F, cfg, st);
   if (rc) return rc;
-  CUDA_TRY(launch_fill(fb->shadow_dev, F.n_pix, 1.0f, ctx->n_sms, st));
+  LAUNCH(ctx, launch_fill(fb->shadow_dev, F.n_pix, 1.0f, ctx->n_sms, st));
   bool shadows = cfg ? cfg->shadows != 0 : true;
   if (shadows) {
     for (int i = 0; i < n_lights; ++i) {
@@ -815,7 +881,7 @@ int nedf_render_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject*
     }
   }
   if (fb->image_dev && F.n_pix > 0)
-    CUDA_TRY(launch_composite(fb->rgb_dev, fb->shadow_dev, fb->image_dev, F.n_pix, ctx->n_sms, st));
+    LAUNCH(ctx, launch_composite(fb->rgb_dev, fb->shadow_dev, fb->image_dev, F.n_pix, ctx->n_sms, st));
   return NEDF_OK;
 }
 

@@ -408,6 +408,8 @@ def compose_frame(scene, camera: Camera, lights, config: RenderConfig | None = N
         "step3_shadow": ev[2].elapsed_time(ev[3]) / 1e3,
         "network_evals": stats["evals"],
         "guarded_evals": stats["guarded"],
+        "kernel_launches": stats["launches"],
+        "h2d_bytes": stats["h2d_bytes"],
     }
     return RenderResult(image=buffers.image, buffers=buffers, timing=timing)
 
