@@ -9,6 +9,7 @@
 
 #include "common.cuh"
 #include "frame.cuh"
+#include "../../include/nedf_b200_diag.h"
 
 using namespace nedf;
 
@@ -775,8 +776,10 @@ int nedf_mlp_forward(NedfContext* ctx, const NedfModel* m, const float* feats, i
 
 static int query_common(NedfContext* ctx, const NedfModel* m, int mode, const double* R, const double* T, double s,
                         const double* o, const double* d, int64_t n, double* depth_or_mu, uint8_t* alpha,
-                        cudaStream_t st) {
-  if (!o || !d || !depth_or_mu || !alpha) return fail(NEDF_ERR_INVALID, "NULL buffer");
+                        cudaStream_t st, float* lc = nullptr, float* lf = nullptr, float* la = nullptr) {
+  const bool logits = lc != nullptr;
+  if (!o || !d || (!logits && (!depth_or_mu || !alpha)) || (logits && (!lf || !la)))
+    return fail(NEDF_ERR_INVALID, "NULL buffer");
   Frame F;
   int rc = single_model_frame(ctx, m, n, F, st);
   if (rc) return rc;
@@ -805,8 +808,25 @@ static int query_common(NedfContext* ctx, const NedfModel* m, int mode, const do
   out.mode = mode == RAY_WORLD ? OUT_QUERY_WORLD : OUT_QUERY_LOCAL;
   if (mode == RAY_WORLD) out.depth = depth_or_mu; else out.mu = depth_or_mu;
   out.alpha = alpha;
+  if (logits) {
+    out.mode = OUT_LOGITS;
+    out.lc = lc; out.lf = lf; out.la = la;
+  }
   LAUNCH(ctx, launch_explicit_setup(job, F.gt, F.ls, out, n, ctx->n_sms, st));
   return run_network(ctx, F, job, out, st);
+}
+
+extern "C" int nedf_diag_ray_logits(NedfContext* ctx, const NedfModel* m, const double* o, const double* d,
+                                    int64_t n, float* lc, float* lf, float* la, int precision, void* stream) {
+  if (!ctx || !m) return fail(NEDF_ERR_INVALID, "NULL argument");
+  if (!lc) return fail(NEDF_ERR_INVALID, "NULL buffer");
+  if (precision == NEDF_PREC_TENSOR && !m->host.tensor_ok) return fail(NEDF_ERR_UNSUPPORTED, "model not tensor-core shaped");
+  int saved = ctx->precision;
+  ctx->precision = precision == NEDF_PREC_TENSOR ? NEDF_PREC_TENSOR : NEDF_PREC_FP32;
+  int rc = query_common(ctx, m, RAY_LOCAL, nullptr, nullptr, 1.0, o, d, n, nullptr, nullptr, (cudaStream_t)stream,
+                        lc, lf, la);
+  ctx->precision = saved;
+  return rc;
 }
 
 int nedf_query_rays(NedfContext* ctx, const NedfModel* m, const double* o, const double* d, int64_t n, double* mu,

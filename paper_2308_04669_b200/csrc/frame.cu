@@ -233,7 +233,7 @@ __global__ void explicit_setup_kernel(RayJob job, GroupTable gt, ListSet ls, Out
       double wo[3], wd[3], lo[3], ld[3], t0, t1;
       item_local_ray(job, (uint32_t)i, 0u, wo, wd, lo, ld);
       hit = slab_clip(lo, ld, m.bmin, m.bmax, t0, t1);
-      if (!hit) {
+      if (!hit && out.mode != OUT_LOGITS) {
         if (out.mode == OUT_QUERY_LOCAL) out.mu[i] = NAN;
         else out.depth[i] = NAN;   // dist - s * NaN
         out.alpha[i] = 0;

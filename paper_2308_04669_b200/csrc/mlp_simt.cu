@@ -96,7 +96,8 @@ __device__ void simt_tile(SimtSmem& S, const DevModel& m, const RayJob& job, con
                           const uint32_t* pix_list, const uint32_t* obj_list, int n_items) {
   const int tid = threadIdx.x;
   const int F = m.d_feat;
-  const bool logits_mode = out.mode == OUT_LOGITS;
+  const bool logits_mode = out.feats != nullptr;          // features given instead of rays
+  const bool logits_out = out.mode == OUT_LOGITS;
   if (tid < kSimtRays) {
     int v = tid < n_items;
     S.valid[tid] = v;
@@ -210,7 +211,7 @@ __device__ void simt_tile(SimtSmem& S, const DevModel& m, const RayJob& job, con
   // ---- decode (model.py:288-292): first maximum wins ----
   if (tid < kSimtRays && S.valid[tid]) {
     const int r = tid;
-    if (logits_mode) {
+    if (logits_out) {
       size_t row = S.pix[r];
       for (int k = 0; k < m.n_coarse; ++k) out.lc[row * m.n_coarse + k] = S.h[r][k];
       for (int k = 0; k < nf; ++k) out.lf[row * nf + k] = S.h[r][128 + k];

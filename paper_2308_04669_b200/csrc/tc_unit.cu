@@ -1,0 +1,105 @@
+// Diagnostic one-CTA tcgen05 GEMM used by the GPU tests to pin the operand
+// layouts the fused network kernel relies on: 128B-swizzled K-major shared
+// tiles (SS form), A staged in TMEM as packed f16x2 columns (TS form), and
+// the 32x32b TMEM load of the fp32 accumulator.
+#include <cstdio>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+#include "../../include/nedf_b200_diag.h"
+
+namespace nedf {
+
+__global__ void __launch_bounds__(128, 1)
+umma_unit_kernel(const __half* __restrict__ A, const __half* __restrict__ B, float* __restrict__ D, int K, int N,
+                 int a_in_tmem, int d_col) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sa = smem;                 // 4 x 16 KB  [128 rows x 64 K] per K chunk
+  unsigned char* sb = smem + 4 * 16384;     // 4 x 32 KB  [256 rows x 64 K]
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nkc = K / 64;
+  // stage A rows (thread = row) and B rows into swizzled tiles
+  for (int kc = 0; kc < nkc; ++kc) {
+    for (int j = 0; j < 8; ++j) {
+      const uint4 v = *reinterpret_cast<const uint4*>(A + (size_t)tid * K + kc * 64 + j * 8);
+      *reinterpret_cast<uint4*>(sa + kc * 16384 + tc::sw128_offset(tid, j)) = v;
+    }
+    for (int r = tid; r < N; r += 128)
+      for (int j = 0; j < 8; ++j) {
+        const uint4 v = *reinterpret_cast<const uint4*>(B + (size_t)r * K + kc * 64 + j * 8);
+        *reinterpret_cast<uint4*>(sb + kc * 32768 + tc::sw128_offset(r, j)) = v;
+      }
+  }
+  tc::fence_proxy_async_smem();
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base_s);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = tmem_base_s;
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  const uint32_t a_col = 256;
+  if (a_in_tmem) {
+    // row tid -> lane tid; column c holds (A[k=2c], A[k=2c+1]) as (lo, hi)
+    for (int c0 = 0; c0 < K / 2; c0 += 16) {
+      uint32_t r[16];
+      for (int j = 0; j < 16; ++j) {
+        __half lo = A[(size_t)tid * K + 2 * (c0 + j)], hi = A[(size_t)tid * K + 2 * (c0 + j) + 1];
+        r[j] = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+      }
+      tc::tmem_st16(tbase + lane_base + a_col + c0, r);
+    }
+    tc::tmem_st_wait();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (tid == 0) {
+    const uint32_t idesc = tc::idesc_f16(128, N);
+    for (int kc = 0; kc < nkc; ++kc)
+      for (int k = 0; k < 4; ++k) {
+        uint64_t bdesc = tc::sw128_desc(tc::smem_u32(sb + kc * 32768) + k * 32);
+        uint32_t acc = (kc | k) ? 1u : 0u;
+        if (a_in_tmem) {
+          tc::mma_ts(tbase + d_col, tbase + a_col + kc * 32 + k * 8, bdesc, idesc, acc);
+        } else {
+          uint64_t adesc = tc::sw128_desc(tc::smem_u32(sa + kc * 16384) + k * 32);
+          tc::mma_ss(tbase + d_col, adesc, bdesc, idesc, acc);
+        }
+      }
+    tc::mma_commit(&bar);
+  }
+  __syncwarp();
+  tc::mbar_wait(&bar, 0);
+  tc::tc_fence_after();
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    uint32_t r[16];
+    tc::tmem_ld16(tbase + lane_base + d_col + c0, r);
+    tc::tmem_ld_wait();
+    for (int j = 0; j < 16; ++j) D[(size_t)tid * N + c0 + j] = __uint_as_float(r[j]);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tbase);
+}
+
+}  // namespace nedf
+
+extern "C" int nedf_diag_umma(const void* a, const void* b, float* d, int k, int n, int a_in_tmem, int d_col,
+                              void* stream) {
+  using namespace nedf;
+  if (!a || !b || !d || k < 64 || k > 256 || k % 64 || n < 16 || n > 256 || n % 16 || d_col < 0 ||
+      d_col + n > 256)
+    return NEDF_ERR_INVALID;
+  size_t smem = 4 * 16384 + 4 * 32768 + 1024;
+  cudaFuncSetAttribute(umma_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  umma_unit_kernel<<<1, 128, smem, (cudaStream_t)stream>>>((const __half*)a, (const __half*)b, d, k, n, a_in_tmem,
+                                                           d_col);
+  return cudaGetLastError() == cudaSuccess ? NEDF_OK : NEDF_ERR_CUDA;
+}
