@@ -27,6 +27,17 @@ int nedf_diag_ray_logits(NedfContext* ctx, const NedfModel* m, const double* ori
                          int64_t n, float* coarse_dev, float* fine_dev, float* alpha_logit_dev, int precision,
                          void* stream);
 
+/* Timeline of CTA 0's second tile in the tensor-core kernel (clock64 stamps):
+ * enable >= 0 sets tracing on/off for later launches; out (host, n <= 1024
+ * entries) receives the stamps: [L] / [40+L] MMA layer start / issued,
+ * [100+8L+s] / [104+8L+s] epilogue slice ready / done, [400+p] / [420+p]
+ * encoder point written / slot acquired, [450+L] producer layer start. */
+int nedf_diag_tc_trace(int enable, unsigned long long* out, int n);
+
+/* tcgen05 issue-rate probe: `iters` M=128 x N MMAs (ts: A from TMEM) from one
+ * warp, committing every `per_commit`; writes elapsed clock64 cycles to out_dev. */
+int nedf_diag_mma_rate(int ts, int n, int iters, int per_commit, unsigned long long* out_dev);
+
 #ifdef __cplusplus
 }
 #endif

@@ -2,27 +2,30 @@
 // (nn.py:115-135) for 128-ray tiles, with the ray encoding produced on chip
 // and the decode / world depth / z-buffer update in the epilogue.
 //
-// Per CTA (one per SM), 16 warps:
+// Per CTA (one per SM), 16 warps in four warpgroups:
 //   warp 0        bulk-copy producer: streams the model's pre-swizzled fp16
-//                 operand image (592 x 8 KB stages per tile) into a 16-stage ring
-//   warp 1        MMA issuer (one thread) + TMEM owner
+//                 operand image (296 x 16 KB stages per tile) into an 8-stage ring
+//   warp 1        MMA issuer (warp-uniform loop, elect.sync issues) + TMEM owner
 //   warps 4-7     encoders: thread = ray; float64 ray setup, 16 sample points,
-//                 sinusoidal features -> fp16 A tiles (128B swizzle) in a 4-stage ring
-//   warps 8-15    epilogue: thread = (ray, 32-column half of each 64-column slice);
-//                 fp32 residual stream x[256] lives in registers (128 per thread)
+//                 sinusoidal features -> fp16 A tiles (128B swizzle), 2-stage ring
+//   warps 8-15    epilogue: thread = (ray, 64-column half of each 128-column slice);
+//                 the fp32 residual stream x[256] lives in registers (128 per thread)
 //
-// TMEM (512 columns): [0,256) fp32 accumulator as four 64-column slices,
-// [256,384) A_P = fp16 x (input of fc1 and the tails), [384,512) A_Q = fp16 h
-// (input of fc2).  Layers after the head use the TS form (A from TMEM).
+// TMEM (512 columns): [0,256) fp32 accumulator as two 128-column slices,
+// [256,384) A_P = fp16 x (input of fc1 and of the tails), [384,512) A_Q = fp16 h
+// (input of fc2).  The head uses the SS form (A = encoded rays in shared
+// memory, N = 256); all later layers use the TS form (A in TMEM, N = 128 per
+// slice), which measured 86% of the nominal tcgen05 rate at N = 128 versus
+// ~75% for the shared-memory-bound SS form.
 //
-// Wavefront: layer L+1's MMA for output slice s, K-slice k waits only for the
-// epilogue of layer L's slice k, so the epilogue of slice k overlaps the MMAs
-// of later slices.
+// Wavefront: layer L+1's MMAs for K chunks 0-1 depend only on the epilogue of
+// layer L's slice 0, so that epilogue overlaps the MMAs of slice 1, and the
+// epilogue of slice 1 overlaps the first half of layer L+1.
 //
-// Precision guard: fp16 operands / fp32 accumulation perturb the logits by
-// ~1e-3 relative; rays whose top-2 coarse or fine margin, or |alpha logit|,
-// is below guard * max|logit| are appended to `redo` and re-evaluated by the
-// fp32 kernel instead of being written here.
+// Precision guard: fp16 operands / fp32 accumulation perturb the logits by up
+// to ~1.2e-3 of max|logit| (scripts/tc_calibrate.py); rays whose top-2 coarse
+// or fine margin, or |alpha logit|, is below guard * max|logit| are appended
+// to `redo` and re-evaluated by the fp32 kernel instead of being written here.
 #include <cstdio>
 #include <vector>
 
@@ -35,15 +38,16 @@ namespace nedf {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kStageBytes = 8192;          // [64 N x 64 K] fp16, 128B swizzle
-constexpr int kStages = 16;
-constexpr int kEncStages = 4;
+constexpr int kStageBytes = 16384;         // [128 N x 64 K] fp16, 128B swizzle
+constexpr int kStages = 8;
+constexpr int kEncStages = 2;
 constexpr int kEncBytes = 16384;           // [128 rows x 64 K] fp16
-constexpr int kHeadStages = 64;            // 16 K chunks x 4 N blocks
-constexpr int kLayerStages = 16;           // 4 N slices x 4 K chunks
+constexpr int kHeadStages = 32;            // 16 points x [256 N x 64 K] (two stages each)
+constexpr int kLayerStages = 8;            // 2 N slices x 4 K chunks
 constexpr int kBodyLayers = 32;
-constexpr int kStagesPerTile = kHeadStages + (kBodyLayers + 1) * kLayerStages;   // 592
+constexpr int kStagesPerTile = kHeadStages + (kBodyLayers + 1) * kLayerStages;   // 296
 constexpr int kBiasLayers = kBodyLayers + 2;                                     // 34
+constexpr int kBiasBytes = kBiasLayers * 256 * 4;
 constexpr uint32_t kAccCol = 0, kAPCol = 256, kAQCol = 384;
 
 struct __align__(16) RowRed {
@@ -55,13 +59,14 @@ struct __align__(16) RowRed {
 struct TcShared {
   uint64_t full[kStages], empty[kStages];
   uint64_t enc_full[kEncStages], enc_empty[kEncStages];
-  uint64_t acc_full[4], epi_done[4];
+  uint64_t acc_full[2], epi_done[2];
   uint32_t tmem_base;
   int tiles[65];
   RowRed red[128][2];
 };
 
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kEncStages * kEncBytes + sizeof(TcShared);
+constexpr size_t kSmemBytes =
+    1024 /*align slack*/ + kStages * kStageBytes + kEncStages * kEncBytes + kBiasBytes + sizeof(TcShared);
 
 __device__ __forceinline__ void tile_lookup(const int* tiles, int ng, int t, const ListSet& ls, int& g,
                                             int64_t& base, int& n) {
@@ -84,7 +89,48 @@ __device__ __forceinline__ void top2_push(float v, int col, float& best, float& 
   }
 }
 
+// Features of one sample coordinate for the fp16 tensor-core path:
+// [p, sin(2^k pi p), cos(2^k pi p)] k = 0..9.  Bases at k = 0 and 5 use the
+// exactly reduced argument (p split into float hi + lo; 2^k p mod 2 is exact
+// for the hi part), then four double-angle steps each; max abs error ~5e-6,
+// well below the fp16 rounding (2.4e-4 at |v| in [0.5, 1)) that follows.
+__device__ __forceinline__ void encode_coord_tc(double p, float out[21]) {
+  const float ph = (float)p;
+  const float pl = (float)(p - (double)ph);
+  out[0] = ph;
+#pragma unroll
+  for (int base = 0; base < kLevels; base += 5) {
+    float r;
+    if (base == 0) {
+      r = ph + pl;
+    } else {
+      const float t = ph * 32.0f;                       // exact
+      r = fmaf(-2.0f, rintf(0.5f * t), t) + 32.0f * pl;  // exact reduction + tail
+    }
+    float s, c;
+    __sincosf(3.14159265358979f * r, &s, &c);
+    out[1 + 2 * base] = s;
+    out[2 + 2 * base] = c;
+#pragma unroll
+    for (int k = base + 1; k < base + 5; ++k) {
+      const float s2 = 2.0f * s * c;
+      const float c2 = (c - s) * (c + s);
+      s = s2;
+      c = c2;
+      out[1 + 2 * k] = s;
+      out[2 + 2 * k] = c;
+    }
+  }
+}
+
 }  // namespace
+
+// optional timeline of CTA 0's second tile (diagnostics, nedf_diag_tc_trace)
+__device__ unsigned long long g_tc_trace[1024];
+__device__ int g_tc_trace_on;
+__device__ __forceinline__ void trace_at(bool on, int idx) {
+  if (on) g_tc_trace[idx] = clock64();
+}
 
 __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
   extern __shared__ unsigned char smem_raw[];
@@ -92,12 +138,15 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* ring = smem;
   unsigned char* enc = ring + kStages * kStageBytes;
-  TcShared& S = *reinterpret_cast<TcShared*>(enc + kEncStages * kEncBytes);
+  float* bias_s = reinterpret_cast<float*>(enc + kEncStages * kEncBytes);
+  TcShared& S = *reinterpret_cast<TcShared*>(enc + kEncStages * kEncBytes + kBiasBytes);
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);    // warp-uniform role index
+  const int lane = tid & 31;
   const ListSet& ls = a.ls;
   const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
+  const bool trace_cta = g_tc_trace_on && blockIdx.x == 0;
 
   if (tid == 0) {
     int cum = 0;
@@ -108,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
     }
     for (int i = 0; i < kStages; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], 1); }
     for (int i = 0; i < kEncStages; ++i) { tc::mbar_init(&S.enc_full[i], 4); tc::mbar_init(&S.enc_empty[i], 1); }
-    for (int i = 0; i < 4; ++i) { tc::mbar_init(&S.acc_full[i], 1); tc::mbar_init(&S.epi_done[i], 8); }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(&S.acc_full[i], 1); tc::mbar_init(&S.epi_done[i], 8); }
     tc::mbar_fence_init();
   }
   if (warp == 1) tc::tmem_alloc<512>(&S.tmem_base);
@@ -120,71 +169,103 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
 
   if (warp < 4) {
     tc::reg_dealloc<40>();
-    if (warp == 0 && lane == 0) {
+    if (warp == 0) {
       // ------------------------------------------------------------------ producer
-      int stage = 0;
+      int stage = 0, ti = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+        const bool tr = trace_cta && ti == 1 && lane == 0;
         int g, n;
         int64_t base;
         tile_lookup(S.tiles, ng, t, ls, g, base, n);
         const unsigned char* w = reinterpret_cast<const unsigned char*>(a.gt.models[g].wpack);
         for (int i = 0; i < kStagesPerTile; ++i) {
           tc::mbar_wait(&S.empty[stage], phase ^ 1);
-          tc::mbar_expect_tx(&S.full[stage], kStageBytes);
-          tc::bulk_g2s(ring + stage * kStageBytes, w + (size_t)i * kStageBytes, kStageBytes, &S.full[stage]);
+          if (i == 0) trace_at(tr, 450);
+          else if (i >= kHeadStages && (i - kHeadStages) % kLayerStages == 0)
+            trace_at(tr, 450 + 1 + (i - kHeadStages) / kLayerStages);
+          if (tc::elect_one()) {
+            tc::mbar_expect_tx(&S.full[stage], kStageBytes);
+            tc::bulk_g2s(ring + stage * kStageBytes, w + (size_t)i * kStageBytes, kStageBytes, &S.full[stage]);
+          }
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
-    } else if (warp == 1 && lane == 0) {
+    } else if (warp == 1) {
       // ------------------------------------------------------------------ MMA issuer
-      int stage = 0, es = 0;
+      int stage = 0, es = 0, ti = 0;
       uint32_t phase = 0, ephase = 0;
       uint32_t layer_ctr = 0;
-      const uint32_t id256 = tc::idesc_f16(128, 256), id64 = tc::idesc_f16(128, 64);
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        // head: A = encoded rays (smem), B = W_head chunk [256 x 64]
-        if (layer_ctr > 0)
-          for (int s = 0; s < 4; ++s) tc::mbar_wait(&S.epi_done[s], (layer_ctr - 1) & 1);
+      const uint32_t id256 = tc::idesc_f16(128, 256), id128 = tc::idesc_f16(128, 128);
+      const uint32_t ring_s = tc::smem_u32(ring), enc_s = tc::smem_u32(enc);
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+        const bool tr = trace_cta && ti == 1 && lane == 0;
+        trace_at(tr, 0);
+        // ---- head (SS): A = encoded rays, B = W_head [256 x 64] per sample point
+        if (layer_ctr > 0) {
+          tc::mbar_wait(&S.epi_done[0], (layer_ctr - 1) & 1);
+          tc::mbar_wait(&S.epi_done[1], (layer_ctr - 1) & 1);
+        }
         for (int c = 0; c < 16; ++c) {
           tc::mbar_wait(&S.enc_full[es], ephase);
-          for (int j = 0; j < 4; ++j) tc::mbar_wait(&S.full[stage + j], phase);
+          tc::mbar_wait(&S.full[stage], phase);
+          tc::mbar_wait(&S.full[stage + 1], phase);
           tc::tc_fence_after();
-          const uint32_t a0 = tc::smem_u32(enc + es * kEncBytes);
-          const uint32_t b0 = tc::smem_u32(ring + stage * kStageBytes);
+          const uint32_t a0 = enc_s + es * kEncBytes, b0 = ring_s + stage * kStageBytes;
+          if (tc::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tc::mma_ss(tbase + kAccCol, tc::sw128_desc(a0 + k * 32), tc::sw128_desc(b0 + k * 32), id256,
-                       (c | k) ? 1u : 0u);
-          for (int j = 0; j < 4; ++j) tc::mma_commit(&S.empty[stage + j]);
-          tc::mma_commit(&S.enc_empty[es]);
-          stage += 4;
+            for (int k = 0; k < 4; ++k)
+              tc::mma_ss(tbase + kAccCol, tc::sw128_desc(a0 + k * 32), tc::sw128_desc(b0 + k * 32), id256,
+                         (c | k) ? 1u : 0u);
+            tc::mma_commit(&S.empty[stage]);
+            tc::mma_commit(&S.empty[stage + 1]);
+            tc::mma_commit(&S.enc_empty[es]);
+          }
+          __syncwarp();
+          stage += 2;
           if (stage == kStages) { stage = 0; phase ^= 1; }
           if (++es == kEncStages) { es = 0; ephase ^= 1; }
         }
-        for (int s = 0; s < 4; ++s) tc::mma_commit(&S.acc_full[s]);
+        if (tc::elect_one()) {
+          tc::mma_commit(&S.acc_full[0]);
+          tc::mma_commit(&S.acc_full[1]);
+        }
+        __syncwarp();
+        trace_at(tr, 40);
         ++layer_ctr;
-        // 32 residual-block layers + the fused tail (TS form, 64-column output slices)
+        // ---- 32 residual-block layers + the fused tail (TS, two 128-column slices)
         for (int L = 1; L <= kBodyLayers + 1; ++L) {
-          const uint32_t a_col = (L & 1) ? kAPCol : (L == kBodyLayers + 1 ? kAPCol : kAQCol);
+          const uint32_t a_col = (L & 1) ? kAPCol : kAQCol;   // fc1 and tail read x, fc2 reads h
           const uint32_t par = (layer_ctr - 1) & 1;
-          uint32_t waited = 0;
-          for (int s = 0; s < 4; ++s) {
-            if (!(waited & (1u << s))) { tc::mbar_wait(&S.epi_done[s], par); waited |= 1u << s; }
+          trace_at(tr, L);
+          tc::mbar_wait(&S.epi_done[0], par);                  // acc slice 0 free, A chunks 0-1 ready
+          bool have1 = false;
+#pragma unroll 1
+          for (int s = 0; s < 2; ++s) {
+#pragma unroll 1
             for (int kc = 0; kc < 4; ++kc) {
-              if (!(waited & (1u << kc))) { tc::mbar_wait(&S.epi_done[kc], par); waited |= 1u << kc; }
+              if (!have1 && (kc >= 2 || s == 1)) {               // acc slice 1 free, A chunks 2-3 ready
+                tc::mbar_wait(&S.epi_done[1], par);
+                have1 = true;
+              }
               tc::mbar_wait(&S.full[stage], phase);
               tc::tc_fence_after();
-              const uint32_t b0 = tc::smem_u32(ring + stage * kStageBytes);
+              const uint32_t b0 = ring_s + stage * kStageBytes;
+              const uint32_t ac = tbase + a_col + kc * 32;
+              if (tc::elect_one()) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                tc::mma_ts(tbase + kAccCol + 64 * s, tbase + a_col + kc * 32 + k * 8, tc::sw128_desc(b0 + k * 32),
-                           id64, (kc | k) ? 1u : 0u);
-              tc::mma_commit(&S.empty[stage]);
+                for (int k = 0; k < 4; ++k)
+                  tc::mma_ts(tbase + kAccCol + 128 * s, ac + k * 8, tc::sw128_desc(b0 + k * 32), id128,
+                             (kc | k) ? 1u : 0u);
+                tc::mma_commit(&S.empty[stage]);
+                if (kc == 3) tc::mma_commit(&S.acc_full[s]);
+              }
+              __syncwarp();
               if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
-            tc::mma_commit(&S.acc_full[s]);
           }
+          trace_at(tr, 40 + L);
           ++layer_ctr;
         }
       }
@@ -193,30 +274,36 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
     tc::reg_dealloc<104>();
     // -------------------------------------------------------------------- encoders
     const int row = tid - 128;
-    int es = 0;
+    int es = 0, ti = 0;
     uint32_t ephase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+      const bool tr = trace_cta && ti == 1 && tid == 128;
       int g, n;
       int64_t base;
       tile_lookup(S.tiles, ng, t, ls, g, base, n);
       const DevModel& m = a.gt.models[g];
       const bool valid = row < n;
-      double lo[3] = {0, 0, 0}, ld[3] = {0, 0, 0}, t0 = 0, t1 = 0;
+      // p(t) = A + t B in the box frame, t = t0 + (t1 - t0) i / 15 (geometry.py:336-340)
+      double pa[3] = {0, 0, 0}, pb[3] = {0, 0, 0}, t0 = 0, t1 = 0;
       if (valid) {
-        double wo[3], wd[3];
+        double wo[3], wd[3], lo[3], ld[3];
         item_local_ray(a.job, ls.pix[base + row], ls.obj[base + row], wo, wd, lo, ld);
         slab_clip(lo, ld, m.bmin, m.bmax, t0, t1);
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          pa[ax] = (lo[ax] - m.c[ax]) / m.h[ax];
+          pb[ax] = ld[ax] / m.h[ax];
+        }
       }
       for (int pt = 0; pt < 16; ++pt) {
         uint32_t packed[32];
         if (valid) {
-          double tt = t0 + (t1 - t0) * lin16(pt);
+          const double tt = t0 + (t1 - t0) * lin16(pt);
           float f[64];
 #pragma unroll
           for (int ax = 0; ax < 3; ++ax) {
-            double p = ((lo[ax] + tt * ld[ax]) - m.c[ax]) / m.h[ax];
             float e[21];
-            encode_coord_fast(p, e);
+            encode_coord_tc(pa[ax] + tt * pb[ax], e);
 #pragma unroll
             for (int j = 0; j < 21; ++j) f[21 * ax + j] = e[j];
           }
@@ -228,6 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
           for (int j = 0; j < 32; ++j) packed[j] = 0u;
         }
         tc::mbar_wait(&S.enc_empty[es], ephase ^ 1);
+        trace_at(tr, 420 + pt);
         unsigned char* dst = enc + es * kEncBytes;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -236,152 +324,193 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
         tc::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&S.enc_full[es]);
+        trace_at(tr, 400 + pt);
         if (++es == kEncStages) { es = 0; ephase ^= 1; }
       }
     }
   } else {
     tc::reg_alloc<184>();
     // -------------------------------------------------------------------- epilogue
-    const int ew = warp - 8;
+    const int ew = warp - 8;                // 0..7
     const int q = warp & 3;                 // TMEM lane quadrant of this warp
-    const int hc = ew >> 2;                 // column half within each 64-column slice
+    const int hc = ew >> 2;                 // 64-column half of each 128-column slice
     const int row = 32 * q + lane;
     const uint32_t lane_addr = tbase + ((uint32_t)(32 * q) << 16);
     uint32_t layer_ctr = 0;
-    float x[4][32];
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    const float* cached_bias = nullptr;
+    float x[2][2][32];                      // [slice][32-column chunk][column]
+    int ti = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+      const bool tr = trace_cta && ti == 1 && tid == 256;
       int g, n;
       int64_t base;
       tile_lookup(S.tiles, ng, t, ls, g, base, n);
       const DevModel& m = a.gt.models[g];
-      const float* bias = m.bias_pack;
+      if (m.bias_pack != cached_bias) {     // stage this model's biases in shared memory
+        const float4* src = reinterpret_cast<const float4*>(m.bias_pack);
+        float4* dst = reinterpret_cast<float4*>(bias_s);
+        for (int i = tid - 256; i < kBiasLayers * 64; i += 256) dst[i] = __ldg(src + i);
+        cached_bias = m.bias_pack;
+        tc::named_bar(1, 256);
+      }
       // ---- head: x = acc + b ----
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const float4* b4 = reinterpret_cast<const float4*>(bias + 64 * s + 32 * hc);
+      for (int s = 0; s < 2; ++s) {
         tc::mbar_wait(&S.acc_full[s], layer_ctr & 1);
         tc::tc_fence_after();
-        uint32_t v[32];
-        tc::tmem_ld32(lane_addr + kAccCol + 64 * s + 32 * hc, v);
-        tc::tmem_ld_wait();
-        uint32_t pk[16];
+        trace_at(tr, 100 + s);
 #pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          float4 b = __ldg(b4 + j4);
-          x[s][4 * j4 + 0] = __uint_as_float(v[4 * j4 + 0]) + b.x;
-          x[s][4 * j4 + 1] = __uint_as_float(v[4 * j4 + 1]) + b.y;
-          x[s][4 * j4 + 2] = __uint_as_float(v[4 * j4 + 2]) + b.z;
-          x[s][4 * j4 + 3] = __uint_as_float(v[4 * j4 + 3]) + b.w;
+        for (int j2 = 0; j2 < 2; ++j2) {
+          const int col = 128 * s + 64 * hc + 32 * j2;
+          const float4* b4 = reinterpret_cast<const float4*>(bias_s + col);
+          uint32_t v[32];
+          tc::tmem_ld32(lane_addr + kAccCol + col, v);
+          tc::tmem_ld_wait();
+          uint32_t pk[16];
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 b = b4[j4];
+            x[s][j2][4 * j4 + 0] = __uint_as_float(v[4 * j4 + 0]) + b.x;
+            x[s][j2][4 * j4 + 1] = __uint_as_float(v[4 * j4 + 1]) + b.y;
+            x[s][j2][4 * j4 + 2] = __uint_as_float(v[4 * j4 + 2]) + b.z;
+            x[s][j2][4 * j4 + 3] = __uint_as_float(v[4 * j4 + 3]) + b.w;
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pk[j] = tc::pack_h2(x[s][j2][2 * j], x[s][j2][2 * j + 1]);
+          tc::tmem_st16(lane_addr + kAPCol + col / 2, pk);
         }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = tc::pack_h2(x[s][2 * j], x[s][2 * j + 1]);
-        tc::tmem_st16(lane_addr + kAPCol + 32 * s + 16 * hc, pk);
         tc::tmem_st_wait();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&S.epi_done[s]);
+        trace_at(tr, 104 + s);
       }
       ++layer_ctr;
       // ---- residual blocks ----
       for (int blk = 0; blk < kBodyLayers / 2; ++blk) {
-        const float* b1 = bias + (size_t)(1 + 2 * blk) * 256;
+        const float* b1 = bias_s + (1 + 2 * blk) * 256;
         const float* b2 = b1 + 256;
+        const int l1 = 1 + 2 * blk;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {     // fc1: h = relu(acc + b1) -> A_Q
-          const float4* b4 = reinterpret_cast<const float4*>(b1 + 64 * s + 32 * hc);
+        for (int s = 0; s < 2; ++s) {     // fc1: h = relu(acc + b1) -> A_Q
           tc::mbar_wait(&S.acc_full[s], layer_ctr & 1);
           tc::tc_fence_after();
-          uint32_t v[32];
-          tc::tmem_ld32(lane_addr + kAccCol + 64 * s + 32 * hc, v);
-          tc::tmem_ld_wait();
-          uint32_t pk[16];
+          trace_at(tr, 100 + l1 * 8 + s);
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            float4 b = __ldg(b4 + j4);
-            pk[2 * j4 + 0] = tc::pack_h2_relu(__uint_as_float(v[4 * j4 + 0]) + b.x, __uint_as_float(v[4 * j4 + 1]) + b.y);
-            pk[2 * j4 + 1] = tc::pack_h2_relu(__uint_as_float(v[4 * j4 + 2]) + b.z, __uint_as_float(v[4 * j4 + 3]) + b.w);
+          for (int j2 = 0; j2 < 2; ++j2) {
+            const int col = 128 * s + 64 * hc + 32 * j2;
+            const float4* b4 = reinterpret_cast<const float4*>(b1 + col);
+            uint32_t v[32];
+            tc::tmem_ld32(lane_addr + kAccCol + col, v);
+            tc::tmem_ld_wait();
+            uint32_t pk[16];
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+              const float4 b = b4[j4];
+              pk[2 * j4 + 0] =
+                  tc::pack_h2_relu(__uint_as_float(v[4 * j4 + 0]) + b.x, __uint_as_float(v[4 * j4 + 1]) + b.y);
+              pk[2 * j4 + 1] =
+                  tc::pack_h2_relu(__uint_as_float(v[4 * j4 + 2]) + b.z, __uint_as_float(v[4 * j4 + 3]) + b.w);
+            }
+            tc::tmem_st16(lane_addr + kAQCol + col / 2, pk);
           }
-          tc::tmem_st16(lane_addr + kAQCol + 32 * s + 16 * hc, pk);
           tc::tmem_st_wait();
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&S.epi_done[s]);
+          trace_at(tr, 104 + l1 * 8 + s);
         }
         ++layer_ctr;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {     // fc2: x += relu(acc + b2) -> A_P = fp16(x)
-          const float4* b4 = reinterpret_cast<const float4*>(b2 + 64 * s + 32 * hc);
+        for (int s = 0; s < 2; ++s) {     // fc2: x += relu(acc + b2) -> A_P = fp16(x)
           tc::mbar_wait(&S.acc_full[s], layer_ctr & 1);
           tc::tc_fence_after();
-          uint32_t v[32];
-          tc::tmem_ld32(lane_addr + kAccCol + 64 * s + 32 * hc, v);
-          tc::tmem_ld_wait();
-          uint32_t pk[16];
+          trace_at(tr, 100 + (l1 + 1) * 8 + s);
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            float4 b = __ldg(b4 + j4);
-            x[s][4 * j4 + 0] += fmaxf(__uint_as_float(v[4 * j4 + 0]) + b.x, 0.f);
-            x[s][4 * j4 + 1] += fmaxf(__uint_as_float(v[4 * j4 + 1]) + b.y, 0.f);
-            x[s][4 * j4 + 2] += fmaxf(__uint_as_float(v[4 * j4 + 2]) + b.z, 0.f);
-            x[s][4 * j4 + 3] += fmaxf(__uint_as_float(v[4 * j4 + 3]) + b.w, 0.f);
+          for (int j2 = 0; j2 < 2; ++j2) {
+            const int col = 128 * s + 64 * hc + 32 * j2;
+            const float4* b4 = reinterpret_cast<const float4*>(b2 + col);
+            uint32_t v[32];
+            tc::tmem_ld32(lane_addr + kAccCol + col, v);
+            tc::tmem_ld_wait();
+            uint32_t pk[16];
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+              const float4 b = b4[j4];
+              x[s][j2][4 * j4 + 0] += fmaxf(__uint_as_float(v[4 * j4 + 0]) + b.x, 0.f);
+              x[s][j2][4 * j4 + 1] += fmaxf(__uint_as_float(v[4 * j4 + 1]) + b.y, 0.f);
+              x[s][j2][4 * j4 + 2] += fmaxf(__uint_as_float(v[4 * j4 + 2]) + b.z, 0.f);
+              x[s][j2][4 * j4 + 3] += fmaxf(__uint_as_float(v[4 * j4 + 3]) + b.w, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) pk[j] = tc::pack_h2(x[s][j2][2 * j], x[s][j2][2 * j + 1]);
+            tc::tmem_st16(lane_addr + kAPCol + col / 2, pk);
           }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) pk[j] = tc::pack_h2(x[s][2 * j], x[s][2 * j + 1]);
-          tc::tmem_st16(lane_addr + kAPCol + 32 * s + 16 * hc, pk);
           tc::tmem_st_wait();
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&S.epi_done[s]);
+          trace_at(tr, 104 + (l1 + 1) * 8 + s);
         }
         ++layer_ctr;
       }
-      // ---- tail: fine = slices 0,1; coarse = slice 2; alpha = slice 3 column 0 ----
-      const float* bt = bias + (size_t)(kBiasLayers - 1) * 256;
+      // ---- tail: slice 0 = fine (128); slice 1 = coarse (cols 0-63), alpha (col 64) ----
+      const float* bt = bias_s + (kBiasLayers - 1) * 256;
       float fbest = -INFINITY, fsecond = -INFINITY, cbest = -INFINITY, csecond = -INFINITY, maxabs = 0.f,
             alpha = 0.f;
       int fidx = 0, cidx = 0;
       bool finite = true;
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const float4* b4 = reinterpret_cast<const float4*>(bt + 64 * s + 32 * hc);
+      for (int s = 0; s < 2; ++s) {
         tc::mbar_wait(&S.acc_full[s], layer_ctr & 1);
         tc::tc_fence_after();
-        uint32_t v[32];
-        tc::tmem_ld32(lane_addr + kAccCol + 64 * s + 32 * hc, v);
-        tc::tmem_ld_wait();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&S.epi_done[s]);
-        if (s < 3) {
+        trace_at(tr, 100 + 33 * 8 + s);
+#pragma unroll
+        for (int j2 = 0; j2 < 2; ++j2) {
+          const int col = 128 * s + 64 * hc + 32 * j2;
+          uint32_t v[32];
+          tc::tmem_ld32(lane_addr + kAccCol + col, v);
+          tc::tmem_ld_wait();
+          if (j2 == 1) {                   // accumulator slice fully read: release it
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&S.epi_done[s]);
+          }
+          if (s == 1 && hc == 1) {         // alpha logit at tail column 192, then padding
+            if (j2 == 0) {
+              alpha = __uint_as_float(v[0]) + bt[192];
+              finite = finite && isfinite(alpha);
+              maxabs = fmaxf(maxabs, fabsf(alpha));
+              if (a.out.mode == OUT_LOGITS && row < n) a.out.la[ls.pix[base + row]] = alpha;
+            }
+            continue;
+          }
+          const float4* b4 = reinterpret_cast<const float4*>(bt + col);
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
-            float4 b = __ldg(b4 + j4);
-            float vv[4] = {__uint_as_float(v[4 * j4]) + b.x, __uint_as_float(v[4 * j4 + 1]) + b.y,
-                           __uint_as_float(v[4 * j4 + 2]) + b.z, __uint_as_float(v[4 * j4 + 3]) + b.w};
+            const float4 b = b4[j4];
+            const float vv[4] = {__uint_as_float(v[4 * j4]) + b.x, __uint_as_float(v[4 * j4 + 1]) + b.y,
+                                 __uint_as_float(v[4 * j4 + 2]) + b.z, __uint_as_float(v[4 * j4 + 3]) + b.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const int col = 64 * s + 32 * hc + 4 * j4 + u;
+              const int c = col + 4 * j4 + u;
               finite = finite && isfinite(vv[u]);
               maxabs = fmaxf(maxabs, fabsf(vv[u]));
-              if (s < 2) top2_push(vv[u], col, fbest, fsecond, fidx);
-              else top2_push(vv[u], col - 128, cbest, csecond, cidx);
+              if (s == 0) top2_push(vv[u], c, fbest, fsecond, fidx);
+              else top2_push(vv[u], c - 128, cbest, csecond, cidx);
             }
             if (a.out.mode == OUT_LOGITS && row < n) {   // diagnostics: raw logits
               const size_t r = ls.pix[base + row];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                const int col = 64 * s + 32 * hc + 4 * j4 + u;
-                if (s < 2) a.out.lf[r * 128 + col] = vv[u];
-                else a.out.lc[r * 64 + col - 128] = vv[u];
+                const int c = col + 4 * j4 + u;
+                if (s == 0) a.out.lf[r * 128 + c] = vv[u];
+                else a.out.lc[r * 64 + c - 128] = vv[u];
               }
             }
           }
-        } else if (hc == 0) {
-          alpha = __uint_as_float(v[0]) + __ldg(bt + 192);
-          finite = finite && isfinite(alpha);
-          maxabs = fmaxf(maxabs, fabsf(alpha));
-          if (a.out.mode == OUT_LOGITS && row < n) a.out.la[ls.pix[base + row]] = alpha;
         }
+        trace_at(tr, 104 + 33 * 8 + s);
       }
       ++layer_ctr;
       RowRed rr;
@@ -391,21 +520,17 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
       tc::named_bar(1, 256);
       if (hc == 0 && row < n) {
         const RowRed o = S.red[row][1];
-        // merge: larger value wins, equal values keep the lower column (ours for fine slice 0 vs 1
-        // interleave is handled by comparing indices)
-        auto merge = [](float b1, float s1, int i1, float b2, float s2, int i2, float& b, float& sec, int& idx) {
-          if (b2 > b1 || (b2 == b1 && i2 < i1)) { b = b2; idx = i2; sec = fmaxf(fmaxf(b1, s1), s2); }
-          else { b = b1; idx = i1; sec = fmaxf(fmaxf(b2, s1), s2); }
-        };
-        float fb, fs, cb, cs;
-        int fi, ci;
-        merge(fbest, fsecond, fidx, o.fbest, o.fsecond, o.fidx, fb, fs, fi);
-        merge(cbest, csecond, cidx, o.cbest, o.csecond, o.cidx, cb, cs, ci);
+        // fine argmax over both halves: larger value wins, ties keep the lower column
+        float fb, fs;
+        int fi;
+        if (o.fbest > fbest) { fb = o.fbest; fi = o.fidx; fs = fmaxf(fmaxf(fbest, fsecond), o.fsecond); }
+        else { fb = fbest; fi = fidx; fs = fmaxf(fmaxf(o.fbest, fsecond), o.fsecond); }
+        const float al = o.alpha;
         const float S_ = fmaxf(rr.maxabs, o.maxabs);
         const float thr = a.guard * S_;
         const uint32_t pix = ls.pix[base + row], obj = ls.obj[base + row];
-        const bool risky = a.use_guard &&
-                           (!(S_ < INFINITY) || (fb - fs) < thr || (cb - cs) < thr || fabsf(alpha) < thr);
+        const bool risky =
+            a.use_guard && (!(S_ < INFINITY) || (fb - fs) < thr || (cbest - csecond) < thr || fabsf(al) < thr);
         if (a.out.mode == OUT_LOGITS) {
           // diagnostics: logits already written
         } else if (risky) {
@@ -415,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
         } else {
           double wo[3], wd[3], lo[3], ld[3];
           item_local_ray(a.job, pix, obj, wo, wd, lo, ld);
-          finish_ray(m, a.job, a.out, pix, obj, ci, fi, (double)alpha, wo, wd);
+          finish_ray(m, a.job, a.out, pix, obj, cidx, fi, (double)al, wo, wd);
         }
       }
       tc::named_bar(1, 256);
@@ -427,6 +552,23 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
 }
 
 bool tc_available() { return true; }
+
+}  // namespace nedf
+
+extern "C" int nedf_diag_tc_trace(int enable, unsigned long long* out, int n) {
+  using namespace nedf;
+  if (enable >= 0) {
+    int v = enable;
+    if (cudaMemcpyToSymbol(g_tc_trace_on, &v, sizeof(int)) != cudaSuccess) return NEDF_ERR_CUDA;
+  }
+  if (out && n > 0) {
+    if (n > 1024) n = 1024;
+    if (cudaMemcpyFromSymbol(out, g_tc_trace, n * sizeof(unsigned long long)) != cudaSuccess) return NEDF_ERR_CUDA;
+  }
+  return NEDF_OK;
+}
+
+namespace nedf {
 
 cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, cudaStream_t stream) {
   static bool configured = false;
@@ -440,10 +582,12 @@ cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-// Pack a paper-shaped model (d_feat 256, 16 blocks) into the stage image the
-// kernel streams: head [16 K chunks][4 N blocks], then per layer
-// [4 N slices][4 K chunks], each stage a 128B-swizzled [64 x 64] fp16 tile;
-// tail rows = fine (0-127), coarse (128-191), alpha (192), zero padding.
+// Pack a paper-shaped model (d_feat 256, 16 blocks, 64/128 bins) into the
+// stage image the kernel streams, each stage a 128B-swizzled [128 x 64] fp16
+// tile: head point c -> stages 2c, 2c+1 (output rows 0-127, 128-255, K = the
+// point's 63 features + 1 zero); layer l -> stages 32 + 8l + 4s + kc (output
+// rows 128s.., K chunk kc); tail rows = fine (0-127), coarse (128-191),
+// alpha (192), zero padding.  Biases: [34 layers][256] fp32, same row order.
 cudaError_t tc_pack_weights(const float* P, int d_in, int F, int n_blocks, int n_coarse, int n_fine,
                             __half** wpack_dev, float** bias_dev, size_t* bytes) {
   if (F != 256 || n_blocks != kBodyLayers / 2 || d_in != kDin || n_coarse != 64 || n_fine != 128)
@@ -454,7 +598,6 @@ cudaError_t tc_pack_weights(const float* P, int d_in, int F, int n_blocks, int n
     size_t off = (size_t)stage * kStageBytes + tc::sw128_offset(r, k >> 3) + (k & 7) * 2;
     img[off / 2] = __float2half_rn(v);
   };
-  // parameter offsets in file order
   size_t p = 0;
   const float* Wh = P + p; p += (size_t)F * d_in;
   const float* bh = P + p; p += F;
@@ -464,32 +607,28 @@ cudaError_t tc_pack_weights(const float* P, int d_in, int F, int n_blocks, int n
   const float* ba = P + p; p += n_coarse + 1;
   const float* Wb = P + p; p += (size_t)n_fine * F;
   const float* bb = P + p; p += n_fine;
-  // head
   for (int c = 0; c < 16; ++c)
-    for (int nb = 0; nb < 4; ++nb)
-      for (int r = 0; r < 64; ++r)
-        for (int k = 0; k < 63; ++k) put(4 * c + nb, r, k, Wh[(size_t)(64 * nb + r) * d_in + 63 * c + k]);
+    for (int n = 0; n < 256; ++n)
+      for (int k = 0; k < 63; ++k) put(2 * c + (n >> 7), n & 127, k, Wh[(size_t)n * d_in + 63 * c + k]);
   for (int o = 0; o < F; ++o) bias[o] = bh[o];
-  // body
   for (int l = 0; l < kBodyLayers; ++l) {
-    int st0 = kHeadStages + l * kLayerStages;
-    for (int s = 0; s < 4; ++s)
+    const int st0 = kHeadStages + l * kLayerStages;
+    for (int s = 0; s < 2; ++s)
       for (int kc = 0; kc < 4; ++kc)
-        for (int r = 0; r < 64; ++r)
-          for (int k = 0; k < 64; ++k) put(st0 + 4 * s + kc, r, k, Wl[l][(size_t)(64 * s + r) * F + 64 * kc + k]);
+        for (int r = 0; r < 128; ++r)
+          for (int k = 0; k < 64; ++k) put(st0 + 4 * s + kc, r, k, Wl[l][(size_t)(128 * s + r) * F + 64 * kc + k]);
     for (int o = 0; o < F; ++o) bias[(size_t)(1 + l) * 256 + o] = bl[l][o];
   }
-  // tail
   auto tail_row = [&](int n) -> const float* {
     if (n < 128) return Wb + (size_t)n * F;
     if (n < 128 + n_coarse + 1) return Wa + (size_t)(n - 128) * F;
     return nullptr;
   };
-  int st0 = kHeadStages + kBodyLayers * kLayerStages;
-  for (int s = 0; s < 4; ++s)
+  const int st0 = kHeadStages + kBodyLayers * kLayerStages;
+  for (int s = 0; s < 2; ++s)
     for (int kc = 0; kc < 4; ++kc)
-      for (int r = 0; r < 64; ++r) {
-        const float* w = tail_row(64 * s + r);
+      for (int r = 0; r < 128; ++r) {
+        const float* w = tail_row(128 * s + r);
         if (!w) continue;
         for (int k = 0; k < 64; ++k) put(st0 + 4 * s + kc, r, k, w[64 * kc + k]);
       }

@@ -103,3 +103,97 @@ extern "C" int nedf_diag_umma(const void* a, const void* b, float* d, int k, int
                                                            d_col);
   return cudaGetLastError() == cudaSuccess ? NEDF_OK : NEDF_ERR_CUDA;
 }
+
+namespace nedf {
+
+// Throughput probe: one thread issues `iters` back-to-back M=128 MMAs of width N
+// (SS: A and B from shared memory; TS: A from TMEM) accumulating into TMEM,
+// and records clock64 from first issue to commit completion.
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int ts, int N, int iters, int per_commit,
+                                                          unsigned long long* out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // warp-uniform for the compiler
+  for (int i = tid; i < (16384 + 32768) / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  tc::fence_proxy_async_smem();
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base_s);
+  if (tid == 0) { tc::mbar_init(&bar, 1); tc::mbar_fence_init(); }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = tmem_base_s;
+  if (warp == 0) {
+    const uint32_t idesc = tc::idesc_f16(128, N);
+    const uint64_t adesc = tc::sw128_desc(tc::smem_u32(smem));
+    const uint64_t bdesc = tc::sw128_desc(tc::smem_u32(smem + 16384));
+    unsigned long long t0 = clock64();
+    uint32_t phase = 0;
+    if (per_commit == -2) {
+      // variant: whole warp runs the loop (uniform values), elect.sync issues
+      for (int i = 0; i < iters; i += 4) {
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t bd = bdesc + 2 * k;
+            const uint64_t ad = adesc + 2 * k;
+            const uint32_t at = tbase + 256 + 8 * k;
+            if (ts) tc::mma_ts(tbase, at, bd, idesc, 1u);
+            else tc::mma_ss(tbase, ad, bd, idesc, 1u);
+          }
+        }
+        __syncwarp();
+      }
+      if (tc::elect_one()) tc::mma_commit(&bar);
+      __syncwarp();
+      tc::mbar_wait(&bar, 0);
+      unsigned long long t1 = clock64();
+      if (tid == 0) out[0] = t1 - t0;
+    } else if (per_commit < 0) {
+      // variant: single thread, unrolled x4 with distinct K offsets, one commit
+      if (tid == 0) {
+        for (int i = 0; i < iters; i += 4) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (ts) tc::mma_ts(tbase, tbase + 256 + 8 * k, bdesc + 2 * k, idesc, 1u);
+            else tc::mma_ss(tbase, adesc + 2 * k, bdesc + 2 * k, idesc, 1u);
+          }
+        }
+        tc::mma_commit(&bar);
+      }
+      __syncwarp();
+      tc::mbar_wait(&bar, 0);
+      unsigned long long t1 = clock64();
+      if (tid == 0) out[0] = t1 - t0;
+    } else
+    for (int i = 0; i < iters; ++i) {
+      if (tc::elect_one()) {
+        if (ts) tc::mma_ts(tbase, tbase + 256, bdesc, idesc, 1u);
+        else tc::mma_ss(tbase, adesc, bdesc, idesc, 1u);
+        if ((i + 1) % per_commit == 0) tc::mma_commit(&bar);
+      }
+      __syncwarp();
+      if ((i + 1) % per_commit == 0 && per_commit < iters) { tc::mbar_wait(&bar, phase); phase ^= 1; }
+    }
+    if (per_commit >= iters) { tc::mbar_wait(&bar, 0); }
+    if (per_commit >= 0) {
+      unsigned long long t1 = clock64();
+      if (tid == 0) out[0] = t1 - t0;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tbase);
+}
+
+}  // namespace nedf
+
+extern "C" int nedf_diag_mma_rate(int ts, int n, int iters, int per_commit, unsigned long long* out_dev) {
+  using namespace nedf;
+  size_t smem = 16384 + 32768 + 1024;
+  cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  mma_rate_kernel<<<1, 128, smem>>>(ts, n, iters, per_commit, out_dev);
+  return cudaGetLastError() == cudaSuccess ? NEDF_OK : NEDF_ERR_CUDA;
+}
