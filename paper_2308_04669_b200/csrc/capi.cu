@@ -57,6 +57,7 @@ struct NedfModel {
   float* bias = nullptr;
   __half* wpack = nullptr;
   float* bias_pack = nullptr;
+  float* wstream = nullptr;
   int device = 0;
 };
 
@@ -379,14 +380,17 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
     if ((rc = prof_mark(ctx, st, 0, false))) return rc;
     if (a.use_guard) {
       if ((rc = prof_mark(ctx, st, 1, true))) return rc;
-      LAUNCH(ctx, launch_mlp_fp32(F.gt, F.redo, job, out, ctx->n_sms, st));
+      LAUNCH(ctx, launch_mlp_fp32_stream(F.gt, F.redo, job, out, ctx->n_sms, 8, st));
       if ((rc = prof_mark(ctx, st, 1, false))) return rc;
     }
     add_counts_kernel<<<1, 32, 0, st>>>(F.ls.count, F.redo.count, F.gt.n_groups, F.fj.stats, a.use_guard);
     ctx->launches += 1;
   } else {
     if ((rc = prof_mark(ctx, st, 0, true))) return rc;
-    LAUNCH(ctx, launch_mlp_fp32(F.gt, F.ls, job, out, ctx->n_sms, st));
+    if (F.sc.all_tc && tc_available() && out.feats == nullptr)
+      LAUNCH(ctx, launch_mlp_fp32_stream(F.gt, F.ls, job, out, ctx->n_sms, 32, st));
+    else
+      LAUNCH(ctx, launch_mlp_fp32(F.gt, F.ls, job, out, ctx->n_sms, st));
     if ((rc = prof_mark(ctx, st, 0, false))) return rc;
     add_counts_kernel<<<1, 32, 0, st>>>(F.ls.count, F.redo.count, F.gt.n_groups, F.fj.stats, 0);
     ctx->launches += 1;
@@ -654,6 +658,9 @@ int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* 
     if (e != cudaSuccess) { cleanup(); return fail(NEDF_ERR_CUDA, std::string("tc pack: ") + cudaGetErrorString(e)); }
     h.wpack = m->wpack;
     h.bias_pack = m->bias_pack;
+    e = fp32_pack_stream(params, info->d_in, F, info->n_blocks, info->n_coarse, info->n_fine, &m->wstream);
+    if (e != cudaSuccess) { cleanup(); return fail(NEDF_ERR_CUDA, std::string("fp32 pack: ") + cudaGetErrorString(e)); }
+    h.wstream = m->wstream;
     h.tensor_ok = 1;
   }
   e = cudaMalloc(&m->dev, sizeof(DevModel));
@@ -699,6 +706,7 @@ void nedf_model_free(NedfModel* m) {
   if (m->bias) cudaFree(m->bias);
   if (m->wpack) cudaFree(m->wpack);
   if (m->bias_pack) cudaFree(m->bias_pack);
+  if (m->wstream) cudaFree(m->wstream);
   if (m->dev) cudaFree(m->dev);
   delete m;
 }

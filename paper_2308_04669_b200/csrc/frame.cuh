@@ -42,6 +42,12 @@ size_t simt_smem_bytes();
 cudaError_t launch_mlp_fp32(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
                             int n_sms, cudaStream_t stream);
 
+// fp32 network with streamed weights (mlp_fp32s.cu), paper-shaped models
+cudaError_t launch_mlp_fp32_stream(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
+                                   int n_sms, int rays_per_cta, cudaStream_t stream);
+cudaError_t fp32_pack_stream(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
+                             float** dev);
+
 // tensor-core network (mlp_tc.cu): evaluates `ls`; with guard > 0, rays whose
 // top-2 margins fall below guard * max|logit| are appended to `redo` instead
 // of being written.
