@@ -38,6 +38,12 @@ int nedf_diag_tc_trace(int enable, unsigned long long* out, int n);
  * warp, committing every `per_commit`; writes elapsed clock64 cycles to out_dev. */
 int nedf_diag_mma_rate(int ts, int n, int iters, int per_commit, unsigned long long* out_dev);
 
+/* L2 -> shared memory bulk-copy bandwidth probe: `ctas` CTAs each stream `total`
+ * bytes of `src` (wrapping within `span`) through `depth` x `stage`-byte
+ * buffers; out_dev[cta] = clock64 cycles. */
+int nedf_diag_bulk_rate(const void* src, size_t span, int stage, int depth, size_t total, int ctas,
+                        unsigned long long* out_dev);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,21 +18,26 @@
 namespace nedf {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;                // 256 output columns x 2 halves of each stage's rows
 constexpr int kRows = 32;                  // input rows per stage
 constexpr int kStageFloats = kRows * 256;
 constexpr int kStageBytes = kStageFloats * 4;
-constexpr int kRing = 4;
 constexpr int kHeadStages = 1024 / kRows;  // 16 points x 64 rows (63 + 1 zero)
 constexpr int kLayerStages = 256 / kRows;
 constexpr int kStreamStages = kHeadStages + 33 * kLayerStages;   // 296
 
+// weight ring depth: as deep as shared memory allows next to the activations
+template <int R>
+constexpr int ring_depth() { return R >= 32 ? 3 : (R >= 16 ? 4 : 5); }
+
 template <int R>
 struct StreamSmem {
+  static constexpr int kRing = ring_depth<R>();
   float ring[kRing][kStageFloats];
   float x[R][256];
   float h[R][256];
   float f[R][64];
+  float part[R][256];            // partial sums of the upper row half
   double ray[R][8];              // pa[3], pb[3], t0, t1
   uint32_t pix[R], obj[R];
   int valid[R];
@@ -44,6 +49,7 @@ struct StreamSmem {
 template <int R>
 __global__ void __launch_bounds__(kThreads, 1)
 mlp_fp32_stream_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
+  constexpr int kRing = StreamSmem<R>::kRing;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StreamSmem<R>& S = *reinterpret_cast<StreamSmem<R>*>(smem_raw);
   __shared__ int s_tiles[65];
@@ -74,12 +80,13 @@ mlp_fp32_stream_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
     const DevModel& m = gt.models[g];
     const float* wimg = m.wstream;
     // prologue: first kRing stages of this tile
-    if (tid == 0)
-      for (int i = 0; i < kRing; ++i) {
-        const int slot = (fill + i) % kRing;
-        tc::mbar_expect_tx(&S.full[slot], kStageBytes);
-        tc::bulk_g2s(S.ring[slot], wimg + (size_t)i * kStageFloats, kStageBytes, &S.full[slot]);
-      }
+    // one issuing thread per ring slot: bulk copies from one thread serialise
+    if (tid < kRing) {
+      const int i = tid;
+      const int slot = (fill + i) % kRing;
+      tc::mbar_expect_tx(&S.full[slot], kStageBytes);
+      tc::bulk_g2s(S.ring[slot], wimg + (size_t)i * kStageFloats, kStageBytes, &S.full[slot]);
+    }
     fill += kRing;
     if (tid < R) {
       const int r = tid;
@@ -103,28 +110,38 @@ mlp_fp32_stream_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
     float acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.f;
-    const int o = tid;
+    const int o = tid & 255, kh = tid >> 8;   // output column, row half of each stage
     for (int i = 0; i < kStreamStages; ++i) {
       // head features for sample point i/2 (float64-accurate, geometry.py:312-342)
       if (i < kHeadStages && (i & 1) == 0) {
         const int pt = i >> 1;
-        for (int e = tid; e < R * 3; e += kThreads) {
-          const int r = e / 3, a = e % 3;
-          double enc[21];
-          if (S.valid[r] && !feats_in) {
-            const double t0 = S.ray[r][6], t1 = S.ray[r][7];
-            const double tt = t0 + (t1 - t0) * lin16(pt);
-            const double p = ((S.ray[r][a] + tt * S.ray[r][3 + a]) - m.c[a]) / m.h[a];
-            encode_coord_f64(p, enc);
-#pragma unroll
-            for (int j = 0; j < 21; ++j) S.f[r][21 * a + j] = (float)enc[j];
-          } else if (S.valid[r]) {
-            for (int j = 0; j < 21; ++j)
-              S.f[r][21 * a + j] = out.feats[(size_t)S.pix[r] * kDin + pt * kPerPoint + 21 * a + j];
-          } else {
-            for (int j = 0; j < 21; ++j) S.f[r][21 * a + j] = 0.f;
+        // one (ray, coordinate, level) per thread: sin/cos(2^k pi p) in float64
+        for (int e = tid; e < R * 3 * 11; e += kThreads) {
+          const int r = e / 33, a = (e / 11) % 3, lev = e % 11;   // lev 10 -> raw p and pad
+          float* dst = &S.f[r][21 * a];
+          if (!S.valid[r]) {
+            if (lev < 10) { dst[1 + 2 * lev] = 0.f; dst[2 + 2 * lev] = 0.f; }
+            else { dst[0] = 0.f; if (a == 0) S.f[r][63] = 0.f; }
+            continue;
           }
-          if (a == 0) S.f[r][63] = 0.f;
+          if (feats_in) {
+            const float* src = out.feats + (size_t)S.pix[r] * kDin + pt * kPerPoint + 21 * a;
+            if (lev < 10) { dst[1 + 2 * lev] = src[1 + 2 * lev]; dst[2 + 2 * lev] = src[2 + 2 * lev]; }
+            else { dst[0] = src[0]; if (a == 0) S.f[r][63] = 0.f; }
+            continue;
+          }
+          const double t0 = S.ray[r][6], t1 = S.ray[r][7];
+          const double tt = t0 + (t1 - t0) * lin16(pt);
+          const double p = ((S.ray[r][a] + tt * S.ray[r][3 + a]) - m.c[a]) / m.h[a];
+          if (lev < 10) {
+            double sn, cs;
+            sincos(p * ldexp(3.141592653589793, lev), &sn, &cs);
+            dst[1 + 2 * lev] = (float)sn;
+            dst[2 + 2 * lev] = (float)cs;
+          } else {
+            dst[0] = (float)p;
+            if (a == 0) S.f[r][63] = 0.f;
+          }
         }
         __syncthreads();
       }
@@ -142,7 +159,7 @@ mlp_fp32_stream_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
         k0 = ((i - kHeadStages) % kLayerStages) * kRows;
       }
 #pragma unroll 4
-      for (int k = 0; k < kRows; k += 4) {
+      for (int k = kh * (kRows / 2); k < (kh + 1) * (kRows / 2); k += 4) {
         const float w0 = W[(k + 0) * 256 + o], w1 = W[(k + 1) * 256 + o];
         const float w2 = W[(k + 2) * 256 + o], w3 = W[(k + 3) * 256 + o];
 #pragma unroll
@@ -156,7 +173,7 @@ mlp_fp32_stream_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       }
       ++used;
       __syncthreads();                       // stage consumed by everyone
-      if (tid == 0 && i + kRing < kStreamStages) {
+      if (tid == (int)(fill % kRing) && i + kRing < kStreamStages) {
         const int fs = fill % kRing;
         tc::mbar_expect_tx(&S.full[fs], kStageBytes);
         tc::bulk_g2s(S.ring[fs], wimg + (size_t)(i + kRing) * kStageFloats, kStageBytes, &S.full[fs]);
@@ -170,19 +187,30 @@ mlp_fp32_stream_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       else if (i >= kHeadStages && (i - kHeadStages) % kLayerStages == kLayerStages - 1)
         layer = (i - kHeadStages) / kLayerStages + 1;
       if (layer >= 0) {
+        if (kh == 1) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) S.part[r][o] = acc[r];
+        }
+        __syncthreads();
         const float b = m.bias_pack[layer * 256 + o];
-        if (layer == 0) {
+        if (kh == 0) {
 #pragma unroll
-          for (int r = 0; r < R; ++r) S.x[r][o] = acc[r] + b;
-        } else if (layer == 33) {
+          for (int r = 0; r < R; ++r) acc[r] += S.part[r][o];
+        }
+        if (kh == 0) {
+          if (layer == 0) {
 #pragma unroll
-          for (int r = 0; r < R; ++r) S.h[r][o] = acc[r] + b;   // logits
-        } else if (layer & 1) {
+            for (int r = 0; r < R; ++r) S.x[r][o] = acc[r] + b;
+          } else if (layer == 33) {
 #pragma unroll
-          for (int r = 0; r < R; ++r) S.h[r][o] = fmaxf(acc[r] + b, 0.f);
-        } else {
+            for (int r = 0; r < R; ++r) S.h[r][o] = acc[r] + b;   // logits
+          } else if (layer & 1) {
 #pragma unroll
-          for (int r = 0; r < R; ++r) S.x[r][o] += fmaxf(acc[r] + b, 0.f);
+            for (int r = 0; r < R; ++r) S.h[r][o] = fmaxf(acc[r] + b, 0.f);
+          } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) S.x[r][o] += fmaxf(acc[r] + b, 0.f);
+          }
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0.f;
@@ -218,6 +246,7 @@ static cudaError_t launch_stream(const GroupTable& gt, const ListSet& ls, const 
                                  int n_sms, cudaStream_t stream) {
   static bool configured = false;
   const size_t smem = sizeof(StreamSmem<R>);
+  static_assert(sizeof(StreamSmem<R>) <= 227 * 1024, "shared memory budget");
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(mlp_fp32_stream_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);

@@ -171,27 +171,33 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
     tc::reg_dealloc<40>();
     if (warp == 0) {
       // ------------------------------------------------------------------ producer
-      int stage = 0, ti = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
-        const bool tr = trace_cta && ti == 1 && lane == 0;
-        int g, n;
-        int64_t base;
-        tile_lookup(S.tiles, ng, t, ls, g, base, n);
-        const unsigned char* w = reinterpret_cast<const unsigned char*>(a.gt.models[g].wpack);
-        for (int i = 0; i < kStagesPerTile; ++i) {
-          tc::mbar_wait(&S.empty[stage], phase ^ 1);
-          if (i == 0) trace_at(tr, 450);
-          else if (i >= kHeadStages && (i - kHeadStages) % kLayerStages == 0)
-            trace_at(tr, 450 + 1 + (i - kHeadStages) / kLayerStages);
-          if (tc::elect_one()) {
-            tc::mbar_expect_tx(&S.full[stage], kStageBytes);
-            tc::bulk_g2s(ring + stage * kStageBytes, w + (size_t)i * kStageBytes, kStageBytes, &S.full[stage]);
+      // Each of the first kStages lanes owns one ring slot and streams the stages
+      // congruent to it: bulk copies issued by one thread serialise (~576
+      // cycles each, scripts/bulk_rate.py), so one issuer per slot keeps
+      // kStages copies in flight.
+      static_assert(kStagesPerTile % kStages == 0, "slots must map to fixed stage residues");
+      if (lane < kStages) {
+        const int slot = lane;
+        uint32_t phase = 0;
+        int ti = 0;
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+          const bool tr = trace_cta && ti == 1 && lane == 0;
+          int g, n;
+          int64_t base;
+          tile_lookup(S.tiles, ng, t, ls, g, base, n);
+          const unsigned char* w = reinterpret_cast<const unsigned char*>(a.gt.models[g].wpack);
+          for (int i = slot; i < kStagesPerTile; i += kStages) {
+            tc::mbar_wait(&S.empty[slot], phase ^ 1);
+            if (i == 0) trace_at(tr, 450);
+            else if (i >= kHeadStages && (i - kHeadStages) % kLayerStages == 0)
+              trace_at(tr, 450 + 1 + (i - kHeadStages) / kLayerStages);
+            tc::mbar_expect_tx(&S.full[slot], kStageBytes);
+            tc::bulk_g2s(ring + slot * kStageBytes, w + (size_t)i * kStageBytes, kStageBytes, &S.full[slot]);
+            phase ^= 1;
           }
-          __syncwarp();
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
+      __syncwarp();
     } else if (warp == 1) {
       // ------------------------------------------------------------------ MMA issuer
       int stage = 0, es = 0, ti = 0;

@@ -197,3 +197,70 @@ extern "C" int nedf_diag_mma_rate(int ts, int n, int iters, int per_commit, unsi
   mma_rate_kernel<<<1, 128, smem>>>(ts, n, iters, per_commit, out_dev);
   return cudaGetLastError() == cudaSuccess ? NEDF_OK : NEDF_ERR_CUDA;
 }
+
+namespace nedf {
+
+// L2 -> shared bulk-copy bandwidth probe: each CTA streams `total` bytes of
+// `src` (wrapping inside `span` bytes) through a ring of `depth` stages of
+// `stage` bytes with cp.async.bulk; out[blockIdx] = cycles taken.
+__global__ void __launch_bounds__(32, 1) bulk_rate_kernel(const unsigned char* src, size_t span, int stage,
+                                                           int depth, size_t total, unsigned long long* out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint64_t bars[16];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 16; ++i) tc::mbar_init(&bars[i], 1);
+    tc::mbar_fence_init();
+  }
+  __syncwarp();
+  const size_t n = total / stage;
+  unsigned long long t0 = clock64();
+  if (depth < 0) {
+    // variant: `-depth` lanes each own one stage and stream independently
+    const int lanes = -depth;
+    if ((int)threadIdx.x < lanes) {
+      const int slot = threadIdx.x;
+      size_t off = ((size_t)(blockIdx.x * 7919 + slot * 131) * stage) % span;
+      uint32_t ph = 0;
+      for (size_t i = slot; i < n; i += lanes) {
+        tc::mbar_expect_tx(&bars[slot], stage);
+        tc::bulk_g2s(smem_raw + (size_t)slot * stage, src + off, stage, &bars[slot]);
+        tc::mbar_wait(&bars[slot], ph);
+        ph ^= 1;
+        off += (size_t)lanes * stage;
+        if (off + stage > span) off = (size_t)slot * stage;
+      }
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) out[blockIdx.x] = clock64() - t0;
+    return;
+  }
+  if (threadIdx.x == 0) {
+    size_t off = ((size_t)blockIdx.x * 7919 * stage) % span;
+    for (size_t i = 0; i < n + depth; ++i) {
+      if (i >= (size_t)depth) {
+        const size_t j = i - depth;
+        tc::mbar_wait(&bars[j % depth], (j / depth) & 1);
+      }
+      if (i < n) {
+        const int slot = i % depth;
+        tc::mbar_expect_tx(&bars[slot], stage);
+        tc::bulk_g2s(smem_raw + (size_t)slot * stage, src + off, stage, &bars[slot]);
+        off += stage;
+        if (off + stage > span) off = 0;
+      }
+    }
+    out[blockIdx.x] = clock64() - t0;
+  }
+}
+
+}  // namespace nedf
+
+extern "C" int nedf_diag_bulk_rate(const void* src, size_t span, int stage, int depth, size_t total, int ctas,
+                                   unsigned long long* out_dev) {
+  using namespace nedf;
+  size_t smem = (size_t)stage * (depth < 0 ? -depth : depth);
+  if (depth > 16 || depth < -16 || smem > 200 * 1024) return NEDF_ERR_INVALID;
+  cudaFuncSetAttribute(bulk_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  bulk_rate_kernel<<<ctas, 32, smem>>>((const unsigned char*)src, span, stage, depth, total, out_dev);
+  return cudaGetLastError() == cudaSuccess ? NEDF_OK : NEDF_ERR_CUDA;
+}
