@@ -212,6 +212,13 @@ int nedf_query_world(NedfContext* ctx, const NedfModel* m, const double R[9], co
 /* STEP 1: depth + id z-buffer over all objects (strict <, earliest scene index wins). */
 int nedf_generation_step(NedfContext* ctx, const NedfCamera* cam, const NedfObject* objs, int n_objs,
                          const NedfField* fields, int n_fields, NedfFrameBuffers* fb, void* stream);
+/* STEP 1 with the per-object plane cache (reuse_buffers, pipeline.py:281-305):
+ * re-evaluate only the objects at scene indices changed_idx[0..n_changed), keep
+ * the other planes in fb->planes_dev (required), then recombine all planes in
+ * scene order with strict < -- bit-identical to a cold STEP 1 with planes. */
+int nedf_reuse_step(NedfContext* ctx, const NedfCamera* cam, const NedfObject* objs, int n_objs,
+                    const NedfField* fields, int n_fields, const int32_t* changed_idx, int n_changed,
+                    NedfFrameBuffers* fb, void* stream);
 /* STEP 2: deferred shading of covered pixels (clear colour elsewhere). */
 int nedf_shading_step(NedfContext* ctx, const NedfCamera* cam, const NedfObject* objs, int n_objs,
                       const NedfField* fields, int n_fields, const NedfRenderConfig* cfg,

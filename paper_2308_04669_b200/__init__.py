@@ -15,7 +15,7 @@ _LAZY = {
     "FrameBuffers": "pipeline", "RenderConfig": "pipeline", "RenderResult": "pipeline",
     "SceneInstance": "pipeline", "PointLight": "pipeline", "DirectionalLight": "pipeline",
     "NedfDepthBackend": "pipeline", "OracleDepthBackend": "pipeline", "FrameRenderer": "pipeline",
-    "generate_primary_rays": "pipeline", "import_external_gbuffer": "pipeline",
+    "generate_primary_rays": "pipeline", "import_external_gbuffer": "pipeline", "reuse_buffers": "pipeline",
     "NedfModel": "model", "load_nedf": "model", "loads_nedf": "model", "save_nedf": "model",
     "new_model": "model", "query_rays": "model", "query_depth_world_batch": "model",
     "RigidTransform": "geometry", "Aabb": "geometry",

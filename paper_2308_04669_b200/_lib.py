@@ -96,6 +96,9 @@ PROTOTYPES = {
     "nedf_query_world": (C.c_int, [P, P, C.POINTER(F64), C.POINTER(F64), F64, P, P, I64, P, P, P]),
     "nedf_generation_step": (C.c_int, [P, C.POINTER(NedfCamera), C.POINTER(NedfObject), C.c_int,
                                        C.POINTER(NedfField), C.c_int, C.POINTER(NedfFrameBuffers), P]),
+    "nedf_reuse_step": (C.c_int, [P, C.POINTER(NedfCamera), C.POINTER(NedfObject), C.c_int,
+                                  C.POINTER(NedfField), C.c_int, C.POINTER(C.c_int32), C.c_int,
+                                  C.POINTER(NedfFrameBuffers), P]),
     "nedf_shading_step": (C.c_int, [P, C.POINTER(NedfCamera), C.POINTER(NedfObject), C.c_int,
                                     C.POINTER(NedfField), C.c_int, C.POINTER(NedfRenderConfig),
                                     C.POINTER(NedfFrameBuffers), P]),

@@ -169,8 +169,7 @@ int build_scene(NedfContext* ctx, const NedfObject* objs, int n_objs, const Nedf
   for (size_t g = 0; g < sc.group_models.size(); ++g) gm[g] = sc.group_models[g]->host;
   CUDA_TRY(ctx->models.ensure(gm.size() * sizeof(DevModel)));
   CUDA_TRY(h2d_async(ctx, ctx->models.ptr, gm.data(), gm.size() * sizeof(DevModel), st));
-  CUDA_TRY(ctx->objs.ensure(sc.objs.size() * sizeof(DevObj)));
-  CUDA_TRY(h2d_async(ctx, ctx->objs.ptr, sc.objs.data(), sc.objs.size() * sizeof(DevObj), st));
+  CUDA_TRY(ctx->objs.ensure(sc.objs.size() * sizeof(DevObj)));   // uploaded by prepare_frame
   if (n_fields > 0) {
     CUDA_TRY(ctx->fields.ensure(n_fields * sizeof(NedfField)));
     CUDA_TRY(h2d_async(ctx, ctx->fields.ptr, fields, n_fields * sizeof(NedfField), st));
@@ -252,7 +251,8 @@ struct Frame {
 };
 
 int prepare_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject* objs, int n_objs,
-                  const NedfField* fields, int n_fields, NedfFrameBuffers* fb, Frame& F, cudaStream_t st) {
+                  const NedfField* fields, int n_fields, NedfFrameBuffers* fb, Frame& F, cudaStream_t st,
+                  const int32_t* recompute_idx = nullptr, int n_recompute = -1) {
   int rc = check_camera(cam);
   if (rc) return rc;
   if (!fb) return fail(NEDF_ERR_INVALID, "frame buffers are NULL");
@@ -262,6 +262,13 @@ int prepare_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject* obj
     double lo[3], hi[3];
     field_bounds(fields, objs[s].radiance_field, lo, hi);
     for (int a = 0; a < 3; ++a) { F.sc.objs[s].rbox_min[a] = lo[a]; F.sc.objs[s].rbox_max[a] = hi[a]; }
+    F.sc.objs[s].recompute = recompute_idx ? 0 : 1;
+  }
+  if (recompute_idx) {
+    for (int k = 0; k < n_recompute; ++k) {
+      if (recompute_idx[k] < 0 || recompute_idx[k] >= n_objs) return fail(NEDF_ERR_INVALID, "recompute index out of range");
+      F.sc.objs[recompute_idx[k]].recompute = 1;
+    }
   }
   if (n_objs > 0)
     CUDA_TRY(h2d_async(ctx, ctx->objs.ptr, F.sc.objs.data(), n_objs * sizeof(DevObj), st));
@@ -413,7 +420,8 @@ int do_step1(NedfContext* ctx, Frame& F, cudaStream_t st) {
   out.plane_stride = F.n_pix;
   int rc = run_network(ctx, F, fj.ray, out, st);
   if (rc) return rc;
-  LAUNCH(ctx, launch_step1_resolve(fj, F.gt, ctx->n_sms, st));
+  if (fj.planes != nullptr) LAUNCH(ctx, launch_recombine(fj, ctx->n_sms, st));   // plane cache kept
+  else LAUNCH(ctx, launch_step1_resolve(fj, F.gt, ctx->n_sms, st));
   return NEDF_OK;
 }
 
@@ -854,6 +862,21 @@ int nedf_generation_step(NedfContext* ctx, const NedfCamera* cam, const NedfObje
   cudaStream_t st = (cudaStream_t)stream;
   Frame F;
   int rc = prepare_frame(ctx, cam, objs, n_objs, fields, n_fields, fb, F, st);
+  if (rc) return rc;
+  return do_step1(ctx, F, st);
+}
+
+int nedf_reuse_step(NedfContext* ctx, const NedfCamera* cam, const NedfObject* objs, int n_objs,
+                    const NedfField* fields, int n_fields, const int32_t* changed_idx, int n_changed,
+                    NedfFrameBuffers* fb, void* stream) {
+  if (!ctx) return fail(NEDF_ERR_INVALID, "context is NULL");
+  if (!fb || !fb->planes_dev) return fail(NEDF_ERR_INVALID, "reuse needs the per-object plane cache (planes_dev)");
+  if (n_changed < 0 || (n_changed > 0 && !changed_idx)) return fail(NEDF_ERR_INVALID, "bad changed list");
+  cudaStream_t st = (cudaStream_t)stream;
+  Frame F;
+  static const int32_t kNone = -1;
+  int rc = prepare_frame(ctx, cam, objs, n_objs, fields, n_fields, fb, F, st, n_changed ? changed_idx : &kNone,
+                         n_changed);
   if (rc) return rc;
   return do_step1(ctx, F, st);
 }

@@ -53,6 +53,8 @@ struct DevObj {
   int pad;
   double rbox_min[3], rbox_max[3];   // appearance bounding box (SceneInstance.sampling_box)
   double sigma_default;             // default_sigma_threshold (pipeline.py:196-199)
+  int recompute;                    // STEP 1 with a plane cache: 1 = evaluate this object's plane
+  int pad2;
 };
 
 struct DevCam {

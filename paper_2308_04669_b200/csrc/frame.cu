@@ -52,6 +52,7 @@ __global__ void setup_kernel(FrameJob fj, GroupTable gt, ListSet ls, int mode) {
     unsigned long long key = kEmptyKey;
     for (int s = 0; s < fj.n_objs; ++s) {
       const DevObj& ob = fj.ray.objs[s];
+      if (mode == RAY_PRIMARY && fj.planes != nullptr && !ob.recompute) continue;   // cached plane kept
       if (ob.depth_kind == NEDF_DEPTH_NEDF) {
         bool hit = false;
         if (live) {
@@ -113,6 +114,26 @@ __global__ void step1_resolve_kernel(FrameJob fj, GroupTable gt) {
     fj.id[p] = fj.ray.objs[sidx].id;
   }
 }
+
+// STEP 1 from per-object planes (_recombine, pipeline.py:259-268): scene order,
+// strict <, so ties go to the earliest object and the result is a pure
+// function of the planes (cached and cold renders are bit-identical).
+__global__ void recombine_kernel(FrameJob fj) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < fj.n_pix; p += stride) {
+    double best = INFINITY;
+    int bs = -1;
+    for (int s = 0; s < fj.n_objs; ++s) {
+      const double v = fj.planes[(size_t)s * fj.n_pix + p];
+      if (v < best) { best = v; bs = s; }
+    }
+    fj.depth[p] = best;
+    fj.id[p] = bs >= 0 ? fj.ray.objs[bs].id : -1;
+    fj.key[p] = bs >= 0 ? pack_key(best, (uint32_t)bs, 0, 0) : kEmptyKey;
+  }
+}
+
+cudaError_t launch_recombine(const FrameJob& fj, int n_sms, cudaStream_t st);
 
 // emission-absorption colour over [t_n, t_f] (fields.py:364-370, 406-420)
 __device__ void volume_color(const NedfField* fields, int root, const double o[3], const double d[3],
@@ -268,6 +289,10 @@ cudaError_t launch_setup(const FrameJob& fj, const GroupTable& gt, const ListSet
 }
 cudaError_t launch_step1_resolve(const FrameJob& fj, const GroupTable& gt, int n_sms, cudaStream_t st) {
   step1_resolve_kernel<<<grid_for(fj.n_pix, n_sms), 256, 0, st>>>(fj, gt);
+  return cudaGetLastError();
+}
+cudaError_t launch_recombine(const FrameJob& fj, int n_sms, cudaStream_t st) {
+  recombine_kernel<<<grid_for(fj.n_pix, n_sms), 256, 0, st>>>(fj);
   return cudaGetLastError();
 }
 cudaError_t launch_shade(const FrameJob& fj, const GroupTable& gt, int n_sms, cudaStream_t st) {

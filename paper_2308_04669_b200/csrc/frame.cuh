@@ -28,6 +28,7 @@ struct FrameJob {
 cudaError_t launch_setup(const FrameJob& fj, const GroupTable& gt, const ListSet& ls, int mode, int n_sms,
                          cudaStream_t st);
 cudaError_t launch_step1_resolve(const FrameJob& fj, const GroupTable& gt, int n_sms, cudaStream_t st);
+cudaError_t launch_recombine(const FrameJob& fj, int n_sms, cudaStream_t st);
 cudaError_t launch_shade(const FrameJob& fj, const GroupTable& gt, int n_sms, cudaStream_t st);
 cudaError_t launch_shadow_resolve(const FrameJob& fj, const GroupTable& gt, int mode, int n_sms, cudaStream_t st);
 cudaError_t launch_fill(float* buf, int64_t n, float v, int n_sms, cudaStream_t st);

@@ -216,6 +216,7 @@ class FrameBuffers:
         self.image = torch.zeros((n_rows, self.width, 3), dtype=torch.float32, device=dev)
         self.keep_planes = keep_planes
         self.planes = None
+        self.plane_ids = None
         self.per_object_depth: dict = {}
 
     def clear_hit_planes(self):
@@ -231,7 +232,7 @@ class FrameBuffers:
         fb.shadow_dev = self.shadow.data_ptr()
         fb.image_dev = self.image.data_ptr()
         if self.keep_planes and n_objs > 0:
-            if self.planes is None or self.planes.shape[0] < n_objs:
+            if self.planes is None or self.planes.shape[0] != n_objs:
                 self.planes = torch.full((n_objs, self.n_rows, self.width), float("inf"), dtype=torch.float64,
                                          device=self.device)
             fb.planes_dev = self.planes.data_ptr()
@@ -320,14 +321,56 @@ def _ctx(buffers):
 
 
 def nedf_generation_step(scene, camera: Camera, buffers: FrameBuffers, _tables=None) -> None:
-    """STEP 1 (pipeline.py:271-278)."""
+    """STEP 1 (pipeline.py:271-278).  With `buffers.keep_planes` every object's
+    alpha-folded depth plane is kept (per_object_depth) and depth/id come from
+    the fp64 strict-< recombine of those planes, so later `reuse_buffers` calls
+    are bit-identical to this cold render."""
     tb = _tables or _SceneTables(scene, buffers.device)
     fb = buffers._c(tb.n_objs)
     _lib.check(_lib.load_library().nedf_generation_step(
         _ctx(buffers).handle, C.byref(camera._c()), tb.objs, tb.n_objs, tb.fields, tb.n_fields, C.byref(fb),
         _lib.stream_handle()))
+    _publish_planes(scene, buffers)
+
+
+def _publish_planes(scene, buffers: FrameBuffers) -> None:
     if buffers.keep_planes:
+        buffers.plane_ids = [inst.id for inst in scene]
         buffers.per_object_depth = {inst.id: buffers.planes[k] for k, inst in enumerate(scene)}
+
+
+def reuse_buffers(scene, camera: Camera, buffers: FrameBuffers, changed_ids, _tables=None) -> dict:
+    """STEP 1 recomputing only the planes of changed objects (pipeline.py:281-305).
+
+    Falls back to a full recompute when an unchanged object has no cached
+    plane.  The recombined result is bit-identical to nedf_generation_step."""
+    import torch
+    changed = set(changed_ids)
+    ids = [inst.id for inst in scene]
+    cached = set(buffers.per_object_depth) if buffers.keep_planes else set()
+    missing = [i for i in ids if i not in changed and i not in cached]
+    if missing or not buffers.keep_planes:
+        buffers.keep_planes = True
+        nedf_generation_step(scene, camera, buffers, _tables)
+        return {"recomputed": ids, "fallback": True}
+    tb = _tables or _SceneTables(scene, buffers.device)
+    if getattr(buffers, "plane_ids", None) != ids:
+        # scene membership / order changed: lay the cached planes out in scene order
+        old = buffers.per_object_depth
+        planes = torch.full((len(ids), buffers.n_rows, buffers.width), float("inf"), dtype=torch.float64,
+                            device=buffers.device)
+        for k, i in enumerate(ids):
+            if i in old and i not in changed:
+                planes[k].copy_(old[i])
+        buffers.planes = planes
+    idx = [k for k, i in enumerate(ids) if i in changed]
+    arr = (C.c_int32 * max(1, len(idx)))(*idx)
+    fb = buffers._c(tb.n_objs)
+    _lib.check(_lib.load_library().nedf_reuse_step(
+        _ctx(buffers).handle, C.byref(camera._c()), tb.objs, tb.n_objs, tb.fields, tb.n_fields, arr, len(idx),
+        C.byref(fb), _lib.stream_handle()))
+    _publish_planes(scene, buffers)
+    return {"recomputed": [ids[k] for k in idx], "fallback": False}
 
 
 def deferred_shading_step(scene, camera: Camera, buffers: FrameBuffers, config: RenderConfig,
@@ -388,7 +431,10 @@ def compose_frame(scene, camera: Camera, lights, config: RenderConfig | None = N
     st = _lib.stream_handle()
     ctx.read_stats(st)
     ev[0].record()
-    nedf_generation_step(scene, camera, buffers, _tables=tb)
+    if changed_ids is None:
+        nedf_generation_step(scene, camera, buffers, _tables=tb)
+    else:
+        reuse_buffers(scene, camera, buffers, changed_ids, _tables=tb)
     ev[1].record()
     if external is not None:
         import_external_gbuffer(buffers, external[0], external[1], external[2])

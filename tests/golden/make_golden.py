@@ -212,7 +212,46 @@ def gen_analytic():
          points=pts, rgb=rgb, sigma=sig)
 
 
+
+
+def gen_extra():
+    """Outlier resampling (pipeline.py:336-350) and voxel appearance
+    (fields.py:294-319, 477-508) on NeDF-backed objects."""
+    spec = cfgs.config4(100, 40)
+    spec.resample = True
+    scene, cam, lights, cfg = ref_scene(spec)
+    res = pipeline.compose_frame(scene, cam, lights, cfg)
+    b = res.buffers
+    save("frame_resample_100x40.npz", depth=b.depth, id=b.id, rgb=b.rgb, shadow=b.shadow, image=res.image,
+         resample_ratio=res.timing["resample_ratio"])
+
+    rng = np.random.default_rng(9)
+    res_ = (6, 5, 7)
+    vf = fields.VoxelField(res_, geometry.Aabb(geometry.vec3(-1.2, -1.0, -1.1), geometry.vec3(1.1, 1.3, 1.0)),
+                           rng.uniform(0, 2, size=res_), rng.uniform(0, 1, size=res_ + (3,)))
+    vox = fields.VoxelOracle(vf)
+    m, _ = paper_model(0, "sphere")
+    sph = fields.AnalyticOracle(fields.Sphere(geometry.vec3(0, 0, 0), 0.6))
+    scene = [pipeline.SceneInstance(3, geometry.RigidTransform(np.eye(3), geometry.vec3(0.0, 0.0, 0.0), 1.0),
+                                    pipeline.NedfDepthBackend(m), vox),
+             pipeline.SceneInstance(5, geometry.RigidTransform(np.eye(3), geometry.vec3(1.2, 0.3, -1.5), 1.0),
+                                    pipeline.OracleDepthBackend(sph), sph)]
+    cam = pipeline.Camera(position=geometry.vec3(0.5, 1.0, -5.0),
+                          orientation=pipeline.look_at([0.5, 1.0, -5.0], [0, 0, 0]), fov_y=0.9, width=64, height=48)
+    light = pipeline.PointLight(geometry.vec3(2.0, 4.0, -3.0), 0.35)
+    out = {}
+    for rs in (False, True):
+        r = pipeline.compose_frame(scene, cam, [light], pipeline.RenderConfig(resample=rs, clear_color=(0.1, 0.2, 0.3)))
+        tag = "rs" if rs else "plain"
+        out[f"depth_{tag}"] = r.buffers.depth
+        out[f"id_{tag}"] = r.buffers.id
+        out[f"image_{tag}"] = r.image
+        out[f"shadow_{tag}"] = r.buffers.shadow
+    save("frame_voxel_mixed_64x48.npz", density=vf.density, color=vf.color, bmin=vf.bounds.min, bmax=vf.bounds.max,
+         **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["geometry", "models", "forward", "analytic", "frames"]
+    which = sys.argv[1:] or ["geometry", "models", "forward", "analytic", "frames", "extra"]
     for w in which:
         globals()[f"gen_{w}"]()

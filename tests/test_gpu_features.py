@@ -1,0 +1,220 @@
+"""GPU tests for the rest of the §8 scope: outlier resampling, voxel
+appearance, the plane cache / reuse_buffers contract, z-buffer tie-breaking,
+degenerate models, full-size frames (subsample parity) and determinism."""
+
+import numpy as np
+import pytest
+
+from oracle import nedf_oracle as O
+from paper_2308_04669_b200 import configs as CF
+from tests.helpers import oracle_model, oracle_scene
+from tests.parity import frame_parity, psnr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2308_04669_b200 as P
+    from paper_2308_04669_b200 import _lib
+    _lib.context().set_option(_lib.OPT_PRECISION, _lib.PREC_AUTO)
+    return P
+
+
+def _mods():
+    from paper_2308_04669_b200 import _lib, fields, geometry, model, pipeline, scenes
+    return _lib, fields, geometry, model, pipeline, scenes
+
+
+def test_resample_matches_reference(P, golden):
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    z = golden("frame_resample_100x40.npz")
+    spec = CF.config4(100, 40)
+    spec.resample = True
+    scene, cam, lights, cfg = scenes.build(spec)
+    res = pipeline.compose_frame(scene, cam, lights, cfg)
+    b = res.buffers.numpy()
+    rep, bad = frame_parity(b["depth"], b["id"], res.image.cpu().numpy(), z["depth"], z["id"], z["image"])
+    assert not bad, (rep, bad)
+    assert res.timing["resample_ratio"] == pytest.approx(float(z["resample_ratio"]), abs=2e-3)
+    np.testing.assert_allclose(b["rgb"], z["rgb"], atol=1e-4)
+
+
+@pytest.mark.parametrize("resample", [False, True])
+def test_voxel_appearance_and_mixed_backends(P, golden, resample):
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    z = golden("frame_voxel_mixed_64x48.npz")
+    vf = fields.VoxelField(z["density"].shape, geometry.Aabb(z["bmin"], z["bmax"]), z["density"], z["color"])
+    vox = fields.VoxelOracle(vf)
+    m = scenes.paper_model(0, "sphere")
+    sph = fields.AnalyticOracle(fields.Sphere(geometry.vec3(0, 0, 0), 0.6))
+    scene = [pipeline.SceneInstance(3, geometry.RigidTransform(np.eye(3), geometry.vec3(0, 0, 0), 1.0),
+                                    pipeline.NedfDepthBackend(m), vox),
+             pipeline.SceneInstance(5, geometry.RigidTransform(np.eye(3), geometry.vec3(1.2, 0.3, -1.5), 1.0),
+                                    pipeline.OracleDepthBackend(sph), sph)]
+    cam = pipeline.Camera(geometry.vec3(0.5, 1.0, -5.0), pipeline.look_at([0.5, 1.0, -5.0], [0, 0, 0]), 0.9, 64, 48)
+    light = pipeline.PointLight(geometry.vec3(2.0, 4.0, -3.0), 0.35)
+    res = pipeline.compose_frame(scene, cam, [light],
+                                 pipeline.RenderConfig(resample=resample, clear_color=(0.1, 0.2, 0.3)))
+    tag = "rs" if resample else "plain"
+    b = res.buffers.numpy()
+    rep, bad = frame_parity(b["depth"], b["id"], res.image.cpu().numpy(), z[f"depth_{tag}"], z[f"id_{tag}"],
+                            z[f"image_{tag}"])
+    assert not bad, (rep, bad)
+    np.testing.assert_allclose(b["shadow"], z[f"shadow_{tag}"], atol=1e-6)
+
+
+def _moved(spec, k, angle):
+    objs = list(spec.objects)
+    o = objs[k]
+    objs[k] = CF.ObjSpec(o.id, o.kind, o.seed, CF.rotation_y(angle) @ o.R, o.T + np.array([0.05, 0.0, 0.0]), o.s)
+    return CF.SceneSpec(spec.name, objs, spec.camera, spec.lights, spec.shadows, spec.resample)
+
+
+def test_reuse_buffers_bit_identical_for_every_subset(P):
+    """test_pipeline.py:339-355 / test_acceptance.py:404-432: moving any subset
+    of objects and recomputing only their planes equals a cold render."""
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    import itertools
+    base = CF.config4(120, 48)
+    base.objects = base.objects[:3]
+    for r in range(1, 4):
+        for subset in itertools.combinations(range(3), r):
+            moved = base
+            for k in subset:
+                moved = _moved(moved, k, 0.3 + 0.1 * k)
+            scene0, cam, lights, cfg = scenes.build(base)
+            scene1, _, _, _ = scenes.build(moved)
+            warm = pipeline.FrameBuffers(cam.width, cam.height, keep_planes=True)
+            pipeline.compose_frame(scene0, cam, lights, cfg, buffers=warm)
+            r_warm = pipeline.compose_frame(scene1, cam, lights, cfg, buffers=warm,
+                                            changed_ids=[scene1[k].id for k in subset])
+            cold = pipeline.FrameBuffers(cam.width, cam.height, keep_planes=True)
+            r_cold = pipeline.compose_frame(scene1, cam, lights, cfg, buffers=cold)
+            a, b = r_warm.buffers.numpy(), r_cold.buffers.numpy()
+            for key in ("depth", "id", "rgb", "shadow"):
+                np.testing.assert_array_equal(a[key], b[key], err_msg=f"{subset} {key}")
+            np.testing.assert_array_equal(r_warm.image.cpu().numpy(), r_cold.image.cpu().numpy())
+
+
+def test_reuse_falls_back_when_cache_missing(P):
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    spec = CF.config4(64, 32)
+    spec.objects = spec.objects[:2]
+    scene, cam, lights, cfg = scenes.build(spec)
+    buf = pipeline.FrameBuffers(cam.width, cam.height)        # no plane cache yet
+    info = pipeline.reuse_buffers(scene, cam, buf, changed_ids=[scene[0].id])
+    assert info["fallback"] is True and info["recomputed"] == [o.id for o in scene]
+    info = pipeline.reuse_buffers(scene, cam, buf, changed_ids=[])
+    assert info == {"recomputed": [], "fallback": False}
+    assert set(buf.per_object_depth) == {o.id for o in scene}
+
+
+def test_zbuffer_ties_go_to_earliest_object(P):
+    """Two copies of one object at the same place: strict < keeps the first
+    (pipeline.py:259-268); the id buffer holds user ids."""
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    spec = CF.config1(48, 48)
+    o = spec.objects[0]
+    spec.objects = [CF.ObjSpec(17, o.kind, o.seed, o.R, o.T, o.s), CF.ObjSpec(4, o.kind, o.seed, o.R, o.T, o.s)]
+    scene, cam, lights, cfg = scenes.build(spec)
+    for keep in (False, True):
+        buf = pipeline.FrameBuffers(cam.width, cam.height, keep_planes=keep)
+        pipeline.nedf_generation_step(scene, cam, buf)
+        ids = buf.id.cpu().numpy()
+        assert set(np.unique(ids)) <= {17, -1}
+        assert (ids == 17).mean() > 0.5
+
+
+def test_zero_weights_decode_to_lowest_bins(P):
+    """test_nn.py:76-85 + test_model.py:253-260: all-zero parameters give zero
+    logits, ties decode to bin 0 (mu = -l) and alpha False (sigma(0) = 0.5)."""
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    om = oracle_model(0, "sphere")
+    zero = O.OracleModel([(np.zeros_like(w), np.zeros_like(b)) for w, b in om.weights], om.half_range,
+                         om.box_min, om.box_max, 0.5)
+    m = model.loads_nedf(O.nedm_bytes(zero))
+    o, d = CF.sweep_rays(256, om.box_min, om.box_max, seed=3)
+    for prec in (_lib.PREC_AUTO, _lib.PREC_FP32):
+        _lib.context().set_option(_lib.OPT_PRECISION, prec)
+        mu, alpha = model.query_rays(m, o, d)
+        np.testing.assert_allclose(mu, -om.half_range, rtol=0, atol=1e-12)
+        assert not alpha.any()
+    _lib.context().set_option(_lib.OPT_PRECISION, _lib.PREC_AUTO)
+
+
+def test_full_size_config4_subsample_parity(P):
+    """The bench workload itself (2000x800, 8 objects, shadows) against the
+    float64 oracle on 4000 random pixels."""
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    spec = CF.config4()
+    scene, cam, lights, cfg = scenes.build(spec)
+    res = pipeline.compose_frame(scene, cam, lights, cfg)
+    b = res.buffers.numpy()
+    img = res.image.cpu().numpy().reshape(-1, 3)
+    pix = np.random.default_rng(7).choice(cam.width * cam.height, size=4000, replace=False)
+    objs, ocam, olights, ocfg = oracle_scene(spec)
+    ref = O.render(objs, ocam, olights, ocfg, pixels=pix, threads=8)
+    rep, bad = frame_parity(b["depth"].ravel()[pix], b["id"].ravel()[pix], img[pix], ref.depth, ref.id, ref.image)
+    assert not bad, (rep, bad)
+    assert res.timing["network_evals"] > 1_000_000
+
+
+def test_frames_are_deterministic(P):
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    scene, cam, lights, cfg = scenes.build(CF.config4(400, 160))
+    r1 = pipeline.compose_frame(scene, cam, lights, cfg)
+    a = r1.buffers.numpy()
+    i1 = r1.image.cpu().numpy()
+    r2 = pipeline.compose_frame(scene, cam, lights, cfg)
+    b = r2.buffers.numpy()
+    for k in ("depth", "id", "rgb", "shadow"):
+        np.testing.assert_array_equal(a[k], b[k])
+    np.testing.assert_array_equal(i1, r2.image.cpu().numpy())
+
+
+def test_precision_modes_agree_on_decisions(P):
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    scene, cam, lights, cfg = scenes.build(CF.config4(300, 120))
+    out = {}
+    for name, prec in (("auto", _lib.PREC_AUTO), ("fp32", _lib.PREC_FP32)):
+        _lib.context().set_option(_lib.OPT_PRECISION, prec)
+        r = pipeline.compose_frame(scene, cam, lights, cfg)
+        out[name] = (r.buffers.numpy(), r.image.cpu().numpy())
+    _lib.context().set_option(_lib.OPT_PRECISION, _lib.PREC_AUTO)
+    (a, ia), (b, ib) = out["auto"], out["fp32"]
+    np.testing.assert_array_equal(a["id"], b["id"])
+    fin = np.isfinite(b["depth"])
+    np.testing.assert_allclose(a["depth"][fin], b["depth"][fin], rtol=0, atol=1e-9)
+    assert psnr(ia, ib) > 80
+
+
+def test_step_timing_report_shape(P):
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    scene, cam, lights, cfg = scenes.build(CF.config4(200, 80))
+    rep = pipeline.step_timing_report(scene, cam, lights, cfg, repetitions=2)
+    assert rep["repetitions"] == 2 and rep["objects"] == 8
+    assert set(rep["steps"]) == {"step1_depth_id", "step2_shading", "step3_shadow"}
+    assert sum(v["share"] for v in rep["steps"].values()) == pytest.approx(1.0)
+
+
+def test_image_tiles_match_full_frame(P):
+    """Multi-GPU partition on one GPU: each rank's stripes rendered with
+    FrameBuffers(rows=...) reassemble to the full frame bit-for-bit."""
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    from paper_2308_04669_b200 import distributed as D
+    scene, cam, lights, cfg = scenes.build(CF.config4(256, 96))
+    full = pipeline.compose_frame(scene, cam, lights, cfg)
+    ref_img = full.image.cpu().numpy()
+    ref = full.buffers.numpy()
+    world = 3
+    img = np.zeros_like(ref_img)
+    ids = np.zeros_like(ref["id"])
+    for r in range(world):
+        rows = D.stripe_rows(cam.height, r, world)
+        buf = pipeline.FrameBuffers(cam.width, cam.height, rows=rows)
+        res = pipeline.compose_frame(scene, cam, lights, cfg, buffers=buf)
+        img[rows] = res.image.cpu().numpy()
+        ids[rows] = buf.id.cpu().numpy()
+    np.testing.assert_array_equal(ids, ref["id"])
+    np.testing.assert_array_equal(img, ref_img)

@@ -141,6 +141,33 @@ def test_voxel_sample(golden):
     np.testing.assert_allclose(sig, z["sigma"], atol=1e-14)
 
 
+def test_resample_frame(golden):
+    z = golden("frame_resample_100x40.npz")
+    spec = C.config4(100, 40)
+    spec.resample = True
+    objs, cam, lights, cfg = oracle_scene(spec)
+    out = O.render(objs, cam, lights, cfg, threads=4)
+    _check_frame(out, z)
+    assert out.resampled / (100 * 40) == pytest.approx(float(z["resample_ratio"]))
+
+
+@pytest.mark.parametrize("tag,resample", [("plain", False), ("rs", True)])
+def test_voxel_mixed_frame(golden, tag, resample):
+    z = golden("frame_voxel_mixed_64x48.npz")
+    vox = ("voxel", z["density"].shape, z["bmin"], z["bmax"], z["density"], z["color"])
+    sph = ("sphere", (0.0, 0.0, 0.0), 0.6)
+    objs = [O.Obj(3, np.eye(3), np.zeros(3), 1.0, vox, model=oracle_model(0, "sphere")),
+            O.Obj(5, np.eye(3), np.array([1.2, 0.3, -1.5]), 1.0, sph)]
+    cam = O.Cam(np.array([0.5, 1.0, -5.0]), O.look_at([0.5, 1.0, -5.0], [0, 0, 0]), 0.9, 64, 48)
+    out = O.render(objs, cam, [O.Light("point", np.array([2.0, 4.0, -3.0]), 0.35)],
+                   O.Config(resample=resample, clear_color=(0.1, 0.2, 0.3)), threads=4)
+    np.testing.assert_array_equal(out.id, z[f"id_{tag}"])
+    fin = np.isfinite(z[f"depth_{tag}"])
+    np.testing.assert_allclose(out.depth[fin], z[f"depth_{tag}"][fin], rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(out.shadow, z[f"shadow_{tag}"])
+    np.testing.assert_allclose(out.image, z[f"image_{tag}"], atol=1e-12)
+
+
 def test_nedm_format_errors():
     m = oracle_model(0, "sphere")
     raw = O.nedm_bytes(m)
