@@ -35,6 +35,14 @@ def test_every_declared_symbol_is_exported(lib):
         assert hasattr(lib, name), name
 
 
+def test_every_header_symbol_is_exported(lib):
+    """All of include/*.h (the public ABI and the diagnostics header)."""
+    for h in sorted((ROOT / "include").glob("*.h")):
+        text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        for name in sorted(set(re.findall(r"\b(nedf_[a-z_]+)\s*\(", text))):
+            assert hasattr(lib, name), f"{h.name}: {name}"
+
+
 def test_python_binding_covers_header():
     from paper_2308_04669_b200 import _lib
     assert sorted(_lib.PROTOTYPES) == declared_functions()
