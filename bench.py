@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="auto", choices=["auto", "tensor", "fp32"])
+    ap.add_argument("--tc-kernel", default="auto", choices=["auto", "single", "pair", "mcast2", "mcast4"])
     ap.add_argument("--width", type=int, default=2000)
     ap.add_argument("--height", type=int, default=800)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -185,6 +186,9 @@ def main():
     ctx.set_option(_lib.OPT_PRECISION, {"auto": _lib.PREC_AUTO, "tensor": _lib.PREC_TENSOR,
                                         "fp32": _lib.PREC_FP32}[args.precision])
     ctx.set_option(_lib.OPT_PROFILE, 1)
+    ctx.set_option(_lib.OPT_TC_KERNEL, {"auto": _lib.TC_AUTO, "single": _lib.TC_SINGLE,
+                                        "pair": _lib.TC_PAIR, "mcast2": _lib.TC_MCAST2,
+                                        "mcast4": _lib.TC_MCAST4}[args.tc_kernel])
     buf = pipeline.FrameBuffers(cam.width, cam.height, device=local, rows=rows)
     rnd = pipeline.FrameRenderer(scene, cam, lights, cfg, buffers=buf)
     stream = torch.cuda.current_stream()
@@ -282,7 +286,8 @@ def main():
     tflops = (evals * FLOP_PER_EVAL) / (net_ms * 1e-3) / 1e12 if net_ms > 0 else 0.0
     roofline = {"bound": "tensor", "achieved": tflops, "peak": burst, "unit": "TFLOP/s",
                 "frac": tflops / burst, "frac_sustained": tflops / sustained, "peak_source": src,
-                "kernel": "nedf_mlp_tc" if ctx.get_option(_lib.OPT_PRECISION) != _lib.PREC_FP32 else "mlp_fp32_kernel",
+                "kernel": ("nedf_mlp_tc2_kernel" if ctx.get_option(_lib.OPT_TC_KERNEL) == _lib.TC_PAIR else "nedf_mlp_tc_kernel")
+                if ctx.get_option(_lib.OPT_PRECISION) != _lib.PREC_FP32 else "mlp_fp32_stream_kernel",
                 "kernel_ms_per_frame": net_ms, "guard_ms_per_frame": guard_ms,
                 "flop_per_eval": FLOP_PER_EVAL, "evals_per_launch": evals / max(1, st["net_launches"] / args.steps),
                 "traffic": None}

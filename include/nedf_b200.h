@@ -62,7 +62,17 @@ enum {
   NEDF_OPT_PRECISION = 1,       /* one of NEDF_PREC_* */
   NEDF_OPT_GUARD_PPM = 2,       /* near-tie guard threshold tau, parts per million of max|logit| */
   NEDF_OPT_TC_CTAS = 3,         /* persistent CTAs for the tensor-core kernel (0 = one per SM) */
-  NEDF_OPT_PROFILE = 4          /* 1 = time every network launch with CUDA events (read back by nedf_read_stats) */
+  NEDF_OPT_PROFILE = 4,         /* 1 = time every network launch with CUDA events (read back by nedf_read_stats) */
+  NEDF_OPT_TC_KERNEL = 5        /* one of NEDF_TC_*: which tensor-core network kernel runs */
+};
+
+/* Tensor-core network kernels (NEDF_OPT_TC_KERNEL). */
+enum {
+  NEDF_TC_AUTO = 0,    /* the fastest measured one (currently NEDF_TC_MCAST2) */
+  NEDF_TC_SINGLE = 1,  /* one CTA per 128-ray tile, M = 128, own weight stream */
+  NEDF_TC_PAIR = 2,    /* CTA pairs (cta_group::2) per 256-ray tile, M = 256, half the weight stream per SM */
+  NEDF_TC_MCAST2 = 3,  /* clusters of 2 CTAs (M = 128 each) sharing one multicast weight stream */
+  NEDF_TC_MCAST4 = 4   /* clusters of 4 CTAs sharing one multicast weight stream */
 };
 
 typedef struct NedfContext NedfContext; /* one per device: streams' scratch, counters */

@@ -67,6 +67,7 @@ struct NedfContext {
   int precision = NEDF_PREC_AUTO;
   int guard_ppm = 3000;
   int tc_ctas = 0;
+  int tc_kernel = NEDF_TC_AUTO;
   int profile = 0;
   int64_t launches = 0;
   // event pairs around network launches (NEDF_OPT_PROFILE); kind 0 = main, 1 = guard
@@ -383,7 +384,12 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
     CUDA_TRY(cudaMemsetAsync(a.tile_counter, 0, 64 * sizeof(int), st));
     int ctas = ctx->tc_ctas > 0 ? ctx->tc_ctas : ctx->n_sms;
     if ((rc = prof_mark(ctx, st, 0, true))) return rc;
-    LAUNCH(ctx, launch_mlp_tc(a, ctas, st));
+    switch (ctx->tc_kernel) {
+      case NEDF_TC_PAIR: LAUNCH(ctx, launch_mlp_tc2(a, ctas, st)); break;
+      case NEDF_TC_SINGLE: LAUNCH(ctx, launch_mlp_tc(a, ctas, 1, st)); break;
+      case NEDF_TC_MCAST4: LAUNCH(ctx, launch_mlp_tc(a, ctas, 4, st)); break;
+      default: LAUNCH(ctx, launch_mlp_tc(a, ctas, 2, st)); break;
+    }
     if ((rc = prof_mark(ctx, st, 0, false))) return rc;
     if (a.use_guard) {
       if ((rc = prof_mark(ctx, st, 1, true))) return rc;
@@ -547,6 +553,10 @@ int nedf_set_option(NedfContext* c, int key, int64_t v) {
     case NEDF_OPT_PROFILE:
       c->profile = v != 0;
       return NEDF_OK;
+    case NEDF_OPT_TC_KERNEL:
+      if (v < NEDF_TC_AUTO || v > NEDF_TC_MCAST4) return fail(NEDF_ERR_INVALID, "bad tensor-core kernel");
+      c->tc_kernel = (int)v;
+      return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }
@@ -558,6 +568,7 @@ int nedf_get_option(NedfContext* c, int key, int64_t* v) {
     case NEDF_OPT_GUARD_PPM: *v = c->guard_ppm; return NEDF_OK;
     case NEDF_OPT_TC_CTAS: *v = c->tc_ctas; return NEDF_OK;
     case NEDF_OPT_PROFILE: *v = c->profile; return NEDF_OK;
+    case NEDF_OPT_TC_KERNEL: *v = c->tc_kernel; return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }

@@ -63,7 +63,10 @@ struct TcArgs {
   int* tile_counter;
 };
 bool tc_available();
-cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, cudaStream_t stream);
+// csize = CTAs per cluster sharing one multicast weight stream (1, 2 or 4)
+cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, int csize, cudaStream_t stream);
+// CTA-pair variant (mlp_tc2.cu): same contract, 256-ray tiles on SM pairs; n_ctas is rounded down to even
+cudaError_t launch_mlp_tc2(const TcArgs& a, int n_ctas, cudaStream_t stream);
 cudaError_t tc_pack_weights(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
                             __half** wpack_dev, float** bias_dev, size_t* bytes);
 

@@ -68,14 +68,15 @@ struct TcShared {
 constexpr size_t kSmemBytes =
     1024 /*align slack*/ + kStages * kStageBytes + kEncStages * kEncBytes + kBiasBytes + sizeof(TcShared);
 
-__device__ __forceinline__ void tile_lookup(const int* tiles, int ng, int t, const ListSet& ls, int& g,
-                                            int64_t& base, int& n) {
+// cluster tile t = (128 * csize) rays of one group; this CTA (cluster rank r) takes rows [128 r, 128 r + 128)
+__device__ __forceinline__ void tile_lookup(const int* tiles, int ng, int t, const ListSet& ls, int csize,
+                                            uint32_t rank, int& g, int64_t& base, int& n) {
   g = 0;
   while (g < ng - 1 && t >= tiles[g + 1]) ++g;
-  int lt = t - tiles[g];
-  n = ls.count[g] - lt * 128;
-  n = n < 128 ? n : 128;
-  base = ls.offset[g] + (int64_t)lt * 128;
+  const int first = (t - tiles[g]) * 128 * csize + 128 * (int)rank;
+  n = ls.count[g] - first;
+  n = n < 0 ? 0 : (n < 128 ? n : 128);
+  base = ls.offset[g] + first;
 }
 
 // argmax bookkeeping: first maximum wins, `second` is the runner-up value
@@ -132,10 +133,16 @@ __device__ __forceinline__ void trace_at(bool on, int idx) {
   if (on) g_tc_trace[idx] = clock64();
 }
 
-__global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
+// csize = CTAs per cluster (1, 2 or 4).  With csize > 1 the CTAs of a cluster
+// run the same model in lockstep and share one weight stream: each CTA's
+// producer fetches 1/csize of every stage and multicasts it into the ring slot
+// of every CTA, so L2 -> SM traffic drops by csize; a slot is refilled once the
+// MMAs of all csize CTAs have released it (multicast commits, empty count csize).
+__global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int csize) {
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting the shared array itself (not via an integer round trip), so the compiler
+  // keeps the shared address space and emits LDS/STS instead of generic loads/stores
+  unsigned char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* ring = smem;
   unsigned char* enc = ring + kStages * kStageBytes;
   float* bias_s = reinterpret_cast<float*>(enc + kEncStages * kEncBytes);
@@ -147,22 +154,26 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
   const ListSet& ls = a.ls;
   const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
   const bool trace_cta = g_tc_trace_on && blockIdx.x == 0;
+  const uint32_t rank = csize > 1 ? tc::cluster_rank() : 0;
+  const int cid = blockIdx.x / csize, n_cl = gridDim.x / csize;
+  const uint16_t cmask = (uint16_t)((1u << csize) - 1);
 
   if (tid == 0) {
     int cum = 0;
     S.tiles[0] = 0;
     for (int g = 0; g < ng; ++g) {
-      cum += (ls.count[g] + 127) / 128;
+      cum += (ls.count[g] + 128 * csize - 1) / (128 * csize);
       S.tiles[g + 1] = cum;
     }
-    for (int i = 0; i < kStages; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], 1); }
+    for (int i = 0; i < kStages; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], csize); }
     for (int i = 0; i < kEncStages; ++i) { tc::mbar_init(&S.enc_full[i], 4); tc::mbar_init(&S.enc_empty[i], 1); }
     for (int i = 0; i < 2; ++i) { tc::mbar_init(&S.acc_full[i], 1); tc::mbar_init(&S.epi_done[i], 8); }
     tc::mbar_fence_init();
   }
   if (warp == 1) tc::tmem_alloc<512>(&S.tmem_base);
   tc::tc_fence_before();
-  __syncthreads();
+  if (csize > 1) tc::cluster_sync();     // peers multicast into this CTA's ring from the first stage on
+  else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = S.tmem_base;
   const int total_tiles = S.tiles[ng];
@@ -180,11 +191,11 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
         const int slot = lane;
         uint32_t phase = 0;
         int ti = 0;
-        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+        for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
           const bool tr = trace_cta && ti == 1 && lane == 0;
           int g, n;
           int64_t base;
-          tile_lookup(S.tiles, ng, t, ls, g, base, n);
+          tile_lookup(S.tiles, ng, t, ls, csize, rank, g, base, n);
           const unsigned char* w = reinterpret_cast<const unsigned char*>(a.gt.models[g].wpack);
           for (int i = slot; i < kStagesPerTile; i += kStages) {
             tc::mbar_wait(&S.empty[slot], phase ^ 1);
@@ -192,7 +203,13 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
             else if (i >= kHeadStages && (i - kHeadStages) % kLayerStages == 0)
               trace_at(tr, 450 + 1 + (i - kHeadStages) / kLayerStages);
             tc::mbar_expect_tx(&S.full[slot], kStageBytes);
-            tc::bulk_g2s(ring + slot * kStageBytes, w + (size_t)i * kStageBytes, kStageBytes, &S.full[slot]);
+            if (csize == 1) {
+              tc::bulk_g2s(ring + slot * kStageBytes, w + (size_t)i * kStageBytes, kStageBytes, &S.full[slot]);
+            } else {
+              const uint32_t part = kStageBytes / csize, off = rank * part;
+              tc::bulk_g2s_multicast(ring + slot * kStageBytes + off, w + (size_t)i * kStageBytes + off, part,
+                                     &S.full[slot], cmask);
+            }
             phase ^= 1;
           }
         }
@@ -205,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
       uint32_t layer_ctr = 0;
       const uint32_t id256 = tc::idesc_f16(128, 256), id128 = tc::idesc_f16(128, 128);
       const uint32_t ring_s = tc::smem_u32(ring), enc_s = tc::smem_u32(enc);
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+      for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
         const bool tr = trace_cta && ti == 1 && lane == 0;
         trace_at(tr, 0);
         // ---- head (SS): A = encoded rays, B = W_head [256 x 64] per sample point
@@ -224,8 +241,8 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
             for (int k = 0; k < 4; ++k)
               tc::mma_ss(tbase + kAccCol, tc::sw128_desc(a0 + k * 32), tc::sw128_desc(b0 + k * 32), id256,
                          (c | k) ? 1u : 0u);
-            tc::mma_commit(&S.empty[stage]);
-            tc::mma_commit(&S.empty[stage + 1]);
+            tc::mma_commit_mc(&S.empty[stage], cmask);
+            tc::mma_commit_mc(&S.empty[stage + 1], cmask);
             tc::mma_commit(&S.enc_empty[es]);
           }
           __syncwarp();
@@ -264,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
                 for (int k = 0; k < 4; ++k)
                   tc::mma_ts(tbase + kAccCol + 128 * s, ac + k * 8, tc::sw128_desc(b0 + k * 32), id128,
                              (kc | k) ? 1u : 0u);
-                tc::mma_commit(&S.empty[stage]);
+                tc::mma_commit_mc(&S.empty[stage], cmask);
                 if (kc == 3) tc::mma_commit(&S.acc_full[s]);
               }
               __syncwarp();
@@ -282,11 +299,11 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
     const int row = tid - 128;
     int es = 0, ti = 0;
     uint32_t ephase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+    for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
       const bool tr = trace_cta && ti == 1 && tid == 128;
       int g, n;
       int64_t base;
-      tile_lookup(S.tiles, ng, t, ls, g, base, n);
+      tile_lookup(S.tiles, ng, t, ls, csize, rank, g, base, n);
       const DevModel& m = a.gt.models[g];
       const bool valid = row < n;
       // p(t) = A + t B in the box frame, t = t0 + (t1 - t0) i / 15 (geometry.py:336-340)
@@ -346,11 +363,11 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
     const float* cached_bias = nullptr;
     float x[2][2][32];                      // [slice][32-column chunk][column]
     int ti = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++ti) {
+    for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
       const bool tr = trace_cta && ti == 1 && tid == 256;
       int g, n;
       int64_t base;
-      tile_lookup(S.tiles, ng, t, ls, g, base, n);
+      tile_lookup(S.tiles, ng, t, ls, csize, rank, g, base, n);
       const DevModel& m = a.gt.models[g];
       if (m.bias_pack != cached_bias) {     // stage this model's biases in shared memory
         const float4* src = reinterpret_cast<const float4*>(m.bias_pack);
@@ -553,7 +570,8 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a) {
     }
   }
   tc::tc_fence_before();
-  __syncthreads();
+  if (csize > 1) tc::cluster_sync();     // no peer may still multicast into / arrive on this CTA
+  else __syncthreads();
   if (warp == 1) tc::tmem_dealloc<512>(tbase);
 }
 
@@ -576,16 +594,43 @@ extern "C" int nedf_diag_tc_trace(int enable, unsigned long long* out, int n) {
 
 namespace nedf {
 
-cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, cudaStream_t stream) {
+cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, int csize, cudaStream_t stream) {
   static bool configured = false;
+  static int max_clusters[5] = {0, 0, 0, 0, 0};
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(nedf_mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kSmemBytes);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  nedf_mlp_tc_kernel<<<n_ctas, kThreads, kSmemBytes, stream>>>(a);
-  return cudaGetLastError();
+  if (csize != 1 && csize != 2 && csize != 4) return cudaErrorInvalidValue;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (csize > 1) {
+    // persistent grid: only as many clusters as can be co-resident (a GPC whose free SM count is
+    // not a multiple of csize leaves SMs idle), or the surplus would run as a second wave
+    if (max_clusters[csize] == 0) {
+      cfg.gridDim = dim3(n_ctas - n_ctas % csize, 1, 1);
+      int n = 0;
+      cudaError_t e = cudaOccupancyMaxActiveClusters(&n, nedf_mlp_tc_kernel, &cfg);
+      if (e != cudaSuccess) return e;
+      max_clusters[csize] = n > 0 ? n : 1;
+    }
+    n_ctas -= n_ctas % csize;
+    if (n_ctas > csize * max_clusters[csize]) n_ctas = csize * max_clusters[csize];
+    if (n_ctas < csize) n_ctas = csize;
+  }
+  cfg.gridDim = dim3(n_ctas, 1, 1);
+  return cudaLaunchKernelEx(&cfg, nedf_mlp_tc_kernel, a, csize);
 }
 
 // Pack a paper-shaped model (d_feat 256, 16 blocks, 64/128 bins) into the

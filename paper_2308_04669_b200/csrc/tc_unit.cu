@@ -109,6 +109,8 @@ namespace nedf {
 // Throughput probe: one thread issues `iters` back-to-back M=128 MMAs of width N
 // (SS: A and B from shared memory; TS: A from TMEM) accumulating into TMEM,
 // and records clock64 from first issue to commit completion.
+__device__ unsigned char g_rate_src[8 * 16384];
+
 __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int ts, int N, int iters, int per_commit,
                                                           unsigned long long* out) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -125,14 +127,65 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int ts, int N, int ite
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = tmem_base_s;
+  __shared__ volatile int stop_flag;
+  if (tid == 0) stop_flag = 0;
+  __syncthreads();
+  if ((per_commit == -5 || per_commit == -6) && warp == 1) {
+    // variant -5: lanes 0-7 of warp 1 stream 16 KB bulk copies global -> shared (L2-resident source)
+    // into a separate 128 KB region while warp 0 issues MMAs: smem write-port contention
+    __shared__ uint64_t cbar[8];
+    const int l = tid & 31;
+    if (l < 8) {
+      tc::mbar_init(&cbar[l], 1);
+      tc::mbar_fence_init();
+      unsigned char* dst = smem + 49152 + l * 16384;
+      uint32_t ph = 0;
+      long long copies = 0;
+      while (!stop_flag) {
+        tc::mbar_expect_tx(&cbar[l], 16384);
+        tc::bulk_g2s(dst, g_rate_src + l * 16384, 16384, &cbar[l]);
+        tc::mbar_wait(&cbar[l], ph);
+        ph ^= 1;
+        ++copies;
+      }
+      if (l == 0) out[1] = copies;
+    }
+    __syncwarp();
+  }
+  if (per_commit <= -3 && per_commit >= -4 && warp != 0) {
+    // variant -3 / -4: the other warps hammer TMEM (-3: tcgen05.ld 32 cols + st 16 cols per round
+    // on columns the MMA does not touch; -4: plain FMA work) while warp 0 issues MMAs
+    const uint32_t lane_addr = tbase + ((uint32_t)(32 * warp) << 16);
+    float acc = 0.f;
+    while (!stop_flag) {
+      if (per_commit == -3) {
+        uint32_t v[32];
+        tc::tmem_ld32(lane_addr + 384, v);
+        tc::tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = v[2 * j] ^ v[2 * j + 1];
+        tc::tmem_st16(lane_addr + 448, pk);
+        tc::tmem_st_wait();
+      } else {
+#pragma unroll 8
+        for (int j = 0; j < 64; ++j) acc = fmaf(acc, 1.0001f, 0.5f);
+      }
+    }
+    if (acc == 12345.f) out[1] = 1;
+  }
   if (warp == 0) {
     const uint32_t idesc = tc::idesc_f16(128, N);
     const uint64_t adesc = tc::sw128_desc(tc::smem_u32(smem));
     const uint64_t bdesc = tc::sw128_desc(tc::smem_u32(smem + 16384));
     unsigned long long t0 = clock64();
     uint32_t phase = 0;
-    if (per_commit == -2) {
+    if (per_commit <= -2) {
       // variant: whole warp runs the loop (uniform values), elect.sync issues
+      if (per_commit == -6) {          // no MMAs: copies alone for iters * 74 cycles
+        while (clock64() - t0 < (unsigned long long)iters * 74) {
+        }
+      } else
       for (int i = 0; i < iters; i += 4) {
         if (tc::elect_one()) {
 #pragma unroll
@@ -151,6 +204,7 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int ts, int N, int ite
       tc::mbar_wait(&bar, 0);
       unsigned long long t1 = clock64();
       if (tid == 0) out[0] = t1 - t0;
+      if (tid == 0) stop_flag = 1;
     } else if (per_commit < 0) {
       // variant: single thread, unrolled x4 with distinct K offsets, one commit
       if (tid == 0) {
@@ -192,7 +246,7 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int ts, int N, int ite
 
 extern "C" int nedf_diag_mma_rate(int ts, int n, int iters, int per_commit, unsigned long long* out_dev) {
   using namespace nedf;
-  size_t smem = 16384 + 32768 + 1024;
+  size_t smem = 16384 + 32768 + 1024 + (per_commit <= -5 ? 8 * 16384 : 0);
   cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   mma_rate_kernel<<<1, 128, smem>>>(ts, n, iters, per_commit, out_dev);
   return cudaGetLastError() == cudaSuccess ? NEDF_OK : NEDF_ERR_CUDA;

@@ -17,6 +17,7 @@ tr = lib.nedf_diag_tc_trace
 tr.restype = C.c_int
 tr.argtypes = [C.c_int, C.POINTER(C.c_ulonglong), C.c_int]
 
+_lib.context().set_option(_lib.OPT_TC_KERNEL, _lib.TC_SINGLE)
 spec = CF.config4()
 scene, cam, lights, cfg = scenes.build(spec)
 buf = pipeline.FrameBuffers(cam.width, cam.height)

@@ -189,6 +189,57 @@ def test_precision_modes_agree_on_decisions(P):
     assert psnr(ia, ib) > 80
 
 
+@pytest.mark.parametrize("prec", ["auto", "tensor"])
+def test_tensor_kernel_variants_agree(P, prec):
+    """Single-CTA, CTA-pair (M = 256, cta_group::2) and cluster-multicast
+    kernels run the same fp16 x fp16 -> fp32 chain; with the guard all must
+    reach the same decisions."""
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    ctx = _lib.context()
+    ctx.set_option(_lib.OPT_PRECISION, {"auto": _lib.PREC_AUTO, "tensor": _lib.PREC_TENSOR}[prec])
+    scene, cam, lights, cfg = scenes.build(CF.config4(300, 120))
+    out = {}
+    for name, k in (("single", _lib.TC_SINGLE), ("pair", _lib.TC_PAIR), ("mcast2", _lib.TC_MCAST2),
+                    ("mcast4", _lib.TC_MCAST4)):
+        ctx.set_option(_lib.OPT_TC_KERNEL, k)
+        r = pipeline.compose_frame(scene, cam, lights, cfg)
+        out[name] = r.buffers.numpy()
+    ctx.set_option(_lib.OPT_TC_KERNEL, _lib.TC_AUTO)
+    ctx.set_option(_lib.OPT_PRECISION, _lib.PREC_AUTO)
+    a = out["single"]
+    for name in ("pair", "mcast2", "mcast4"):
+        b = out[name]
+        same = a["id"] == b["id"]
+        if prec == "auto" or name != "pair":
+            # the multicast kernels run the identical per-CTA MMA sequence: bit-identical
+            assert same.all(), name
+            fin = np.isfinite(a["depth"])
+            np.testing.assert_allclose(a["depth"][fin], b["depth"][fin], rtol=0, atol=1e-9)
+        else:
+            assert same.mean() > 0.999
+
+
+def test_cluster_kernels_ragged_group_tails(P):
+    """Group sizes that leave later CTAs of a pair / cluster with 0, 1 or 127 rays."""
+    _lib, fields, geometry, model, pipeline, scenes = _mods()
+    ctx = _lib.context()
+    m = scenes.paper_model(0, "sphere")
+    rng = np.random.default_rng(7)
+    for n in (1, 127, 128, 129, 255, 256, 257, 383, 1000):
+        o = rng.normal(size=(n, 3)) * 0.2 + np.array([0.0, 0.0, -3.0])
+        d = np.tile([0.0, 0.0, 1.0], (n, 1)) + rng.normal(size=(n, 3)) * 0.05
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        res = {}
+        kernels = (_lib.TC_SINGLE, _lib.TC_PAIR, _lib.TC_MCAST2, _lib.TC_MCAST4)
+        for k in kernels:
+            ctx.set_option(_lib.OPT_TC_KERNEL, k)
+            res[k] = model.query_rays(m, o, d)
+        ctx.set_option(_lib.OPT_TC_KERNEL, _lib.TC_AUTO)
+        for k in kernels[1:]:
+            np.testing.assert_array_equal(res[_lib.TC_SINGLE][0], res[k][0])
+            np.testing.assert_array_equal(res[_lib.TC_SINGLE][1], res[k][1])
+
+
 def test_step_timing_report_shape(P):
     _lib, fields, geometry, model, pipeline, scenes = _mods()
     scene, cam, lights, cfg = scenes.build(CF.config4(200, 80))
