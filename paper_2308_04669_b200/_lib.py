@@ -122,7 +122,8 @@ def load_library(path: Path | str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # NEDF_LIB: load an alternative build (timing experiments); still the native library, no fallback
+        p = Path(path) if path else Path(os.environ.get("NEDF_LIB", LIB_PATH))
         if not p.exists():
             raise RuntimeError(f"{p} not built: run `python -m paper_2308_04669_b200.build` "
                                "(there is no CPU fallback)")

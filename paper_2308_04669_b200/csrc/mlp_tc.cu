@@ -132,6 +132,19 @@ __device__ int g_tc_trace_on;
 __device__ __forceinline__ void trace_at(bool on, int idx) {
   if (on) g_tc_trace[idx] = clock64();
 }
+// wait, accumulating the cycles spent when tracing
+#ifndef NEDF_TC_SPIN
+#define NEDF_TC_SPIN 1
+#endif
+__device__ __forceinline__ void twait(uint64_t* bar, uint32_t ph, bool on, unsigned long long& acc) {
+  if (on) {
+    const long long t0 = clock64();
+    if (NEDF_TC_SPIN) tc::mbar_spin(bar, ph); else tc::mbar_wait(bar, ph);
+    acc += clock64() - t0;
+  } else {
+    if (NEDF_TC_SPIN) tc::mbar_spin(bar, ph); else tc::mbar_wait(bar, ph);
+  }
+}
 
 // csize = CTAs per cluster (1, 2 or 4).  With csize > 1 the CTAs of a cluster
 // run the same model in lockstep and share one weight stream: each CTA's
@@ -198,7 +211,8 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           tile_lookup(S.tiles, ng, t, ls, csize, rank, g, base, n);
           const unsigned char* w = reinterpret_cast<const unsigned char*>(a.gt.models[g].wpack);
           for (int i = slot; i < kStagesPerTile; i += kStages) {
-            tc::mbar_wait(&S.empty[slot], phase ^ 1);
+            if (NEDF_TC_SPIN) tc::mbar_spin(&S.empty[slot], phase ^ 1);
+            else tc::mbar_wait(&S.empty[slot], phase ^ 1);
             if (i == 0) trace_at(tr, 450);
             else if (i >= kHeadStages && (i - kHeadStages) % kLayerStages == 0)
               trace_at(tr, 450 + 1 + (i - kHeadStages) / kLayerStages);
@@ -224,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
       const uint32_t ring_s = tc::smem_u32(ring), enc_s = tc::smem_u32(enc);
       for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
         const bool tr = trace_cta && ti == 1 && lane == 0;
+        unsigned long long w_full = 0, w_epi = 0, w_enc = 0;
         trace_at(tr, 0);
         // ---- head (SS): A = encoded rays, B = W_head [256 x 64] per sample point
         if (layer_ctr > 0) {
@@ -231,9 +246,9 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           tc::mbar_wait(&S.epi_done[1], (layer_ctr - 1) & 1);
         }
         for (int c = 0; c < 16; ++c) {
-          tc::mbar_wait(&S.enc_full[es], ephase);
-          tc::mbar_wait(&S.full[stage], phase);
-          tc::mbar_wait(&S.full[stage + 1], phase);
+          twait(&S.enc_full[es], ephase, tr, w_enc);
+          twait(&S.full[stage], phase, tr, w_full);
+          twait(&S.full[stage + 1], phase, tr, w_full);
           tc::tc_fence_after();
           const uint32_t a0 = enc_s + es * kEncBytes, b0 = ring_s + stage * kStageBytes;
           if (tc::elect_one()) {
@@ -262,17 +277,17 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           const uint32_t a_col = (L & 1) ? kAPCol : kAQCol;   // fc1 and tail read x, fc2 reads h
           const uint32_t par = (layer_ctr - 1) & 1;
           trace_at(tr, L);
-          tc::mbar_wait(&S.epi_done[0], par);                  // acc slice 0 free, A chunks 0-1 ready
+          twait(&S.epi_done[0], par, tr, w_epi);               // acc slice 0 free, A chunks 0-1 ready
           bool have1 = false;
 #pragma unroll 1
           for (int s = 0; s < 2; ++s) {
 #pragma unroll 1
             for (int kc = 0; kc < 4; ++kc) {
               if (!have1 && (kc >= 2 || s == 1)) {               // acc slice 1 free, A chunks 2-3 ready
-                tc::mbar_wait(&S.epi_done[1], par);
+                twait(&S.epi_done[1], par, tr, w_epi);
                 have1 = true;
               }
-              tc::mbar_wait(&S.full[stage], phase);
+              twait(&S.full[stage], phase, tr, w_full);
               tc::tc_fence_after();
               const uint32_t b0 = ring_s + stage * kStageBytes;
               const uint32_t ac = tbase + a_col + kc * 32;
@@ -290,6 +305,11 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           }
           trace_at(tr, 40 + L);
           ++layer_ctr;
+        }
+        if (tr) {
+          g_tc_trace[600] = w_full;
+          g_tc_trace[601] = w_epi;
+          g_tc_trace[602] = w_enc;
         }
       }
     }

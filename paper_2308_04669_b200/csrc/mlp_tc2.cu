@@ -119,6 +119,11 @@ __device__ __forceinline__ void encode_coord_tc(double p, float out[21]) {
 // [8+r] producer lane 0 of CTA r waiting on empty, [10] follower relay wait on full,
 // [12+r] encoder warp 4 of CTA r waiting on enc_empty, [14+r] encoder tile cycles,
 // [16+r] epilogue warp 8 of CTA r waiting on acc_full, [18+r] epilogue tile cycles
+// timing experiments only (results invalid): 1 = skip the peer_full relay wait, 2 = leader ignores the odd
+// CTA's epilogue
+#ifndef NEDF_PAIR_EXP
+#define NEDF_PAIR_EXP 0
+#endif
 __device__ unsigned long long g_tc2_trace[512];
 __device__ int g_tc2_trace_on;
 
@@ -163,7 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) nedf_ml
       tc::mbar_init(&S.empty[i], 1);
     }
     for (int i = 0; i < kEncStages; ++i) { tc::mbar_init(&S.enc_full[i], 8); tc::mbar_init(&S.enc_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { tc::mbar_init(&S.acc_full[i], 1); tc::mbar_init(&S.epi_done[i], 16); }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(&S.acc_full[i], 1); tc::mbar_init(&S.epi_done[i], (NEDF_PAIR_EXP & 2) ? 8 : 16); }
     tc::mbar_fence_init();
   }
   if (warp == 1) tc::tmem_alloc2<512>(&S.tmem_base);
@@ -240,8 +245,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) nedf_ml
           twait(&S.enc_full[es], ephase, tr, wn);
           twait(&S.full[slot], ph, tr, wf);
           twait(&S.full[slot + 1], ph, tr, wf);
-          twait(&S.peer_full[slot], ph, tr, wp);
-          twait(&S.peer_full[slot + 1], ph, tr, wp);
+          if (!(NEDF_PAIR_EXP & 1)) {
+            twait(&S.peer_full[slot], ph, tr, wp);
+            twait(&S.peer_full[slot + 1], ph, tr, wp);
+          }
           tc::tc_fence_after();
           const uint32_t a0 = enc_s + es * kEncBytes, b0 = ring_s + slot * kUnitBytes;
           if (tc::elect_one()) {
@@ -280,7 +287,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) nedf_ml
               }
               const uint32_t slot = gs % kRing, ph = (gs / kRing) & 1;
               twait(&S.full[slot], ph, tr, wf);
-              twait(&S.peer_full[slot], ph, tr, wp);
+              if (!(NEDF_PAIR_EXP & 1)) twait(&S.peer_full[slot], ph, tr, wp);
               tc::tc_fence_after();
               const uint32_t b0 = ring_s + slot * kUnitBytes;
               const uint32_t ac = tbase + a_col + kc * 32;
@@ -408,7 +415,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) nedf_ml
       auto release = [&](int s) {          // slice s of this CTA's accumulator / A operand is done
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive_remote(leader_epi0 + s * (uint32_t)sizeof(uint64_t));
+        if (lane == 0 && (!(NEDF_PAIR_EXP & 2) || rank == 0))
+          tc::mbar_arrive_remote(leader_epi0 + s * (uint32_t)sizeof(uint64_t));
         if (tr0) g_tc2_trace[204 + 2 * (layer_ctr - layer0) + s] = clock64();
       };
       // ---- head: x = acc + b ----

@@ -189,8 +189,11 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int ts, int N, int ite
       for (int i = 0; i < iters; i += 4) {
         if (tc::elect_one()) {
 #pragma unroll
+          // variant -7: B cycles through eight 16 KB slots (no operand reuse between stages)
+          const uint64_t bslot =
+              per_commit == -7 ? tc::sw128_desc(tc::smem_u32(smem + 49152 + ((i >> 2) & 7) * 16384)) : bdesc;
           for (int k = 0; k < 4; ++k) {
-            const uint64_t bd = bdesc + 2 * k;
+            const uint64_t bd = bslot + 2 * k;
             const uint64_t ad = adesc + 2 * k;
             const uint32_t at = tbase + 256 + 8 * k;
             if (ts) tc::mma_ts(tbase, at, bd, idesc, 1u);

@@ -98,7 +98,8 @@ mma2_rate_kernel(int ts, int N, int iters, unsigned long long* out) {
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const uint32_t rank = tc::cluster_rank();
-  for (int i = tid; i < (16384 + 32768) / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < ((ts & 2) ? 16384 + 32768 + 8 * 16384 : 16384 + 32768) / 16; i += 128)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
   tc::fence_proxy_async_smem();
   if (warp == 0) tc::tmem_alloc2<512>(&tmem_base_s);
   if (tid == 0) { tc::mbar_init(&bar, 1); tc::mbar_fence_init(); }
@@ -115,8 +116,10 @@ mma2_rate_kernel(int ts, int N, int iters, unsigned long long* out) {
       if (tc::elect_one()) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          if (ts) tc::mma2_ts(tbase, tbase + 256 + 8 * k, bdesc + 2 * k, idesc, 1u);
-          else tc::mma2_ss(tbase, adesc + 2 * k, bdesc + 2 * k, idesc, 1u);
+          // ts & 2: B cycles through eight 16 KB slots (no operand reuse between stages)
+          const uint64_t bd = (ts & 2) ? tc::sw128_desc(tc::smem_u32(smem + 49152 + ((i >> 2) & 7) * 16384)) : bdesc;
+          if (ts & 1) tc::mma2_ts(tbase, tbase + 256 + 8 * k, bd + 2 * k, idesc, 1u);
+          else tc::mma2_ss(tbase, adesc + 2 * k, bd + 2 * k, idesc, 1u);
         }
       }
       __syncwarp();
@@ -139,7 +142,7 @@ mma2_rate_kernel(int ts, int N, int iters, unsigned long long* out) {
 extern "C" int nedf_diag_mma2_rate(int ts, int n, int iters, unsigned long long* out_dev) {
   using namespace nedf;
   if (!out_dev || n < 32 || n > 256 || n % 32 || iters < 4) return NEDF_ERR_INVALID;
-  const size_t smem = 16384 + 32768 + 1024;
+  const size_t smem = 16384 + 32768 + 1024 + ((ts & 2) ? 8 * 16384 : 0);
   cudaFuncSetAttribute(mma2_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   mma2_rate_kernel<<<2, 128, smem>>>(ts, n, iters, out_dev);
   return cudaGetLastError() == cudaSuccess ? NEDF_OK : NEDF_ERR_CUDA;
