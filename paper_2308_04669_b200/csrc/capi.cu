@@ -58,6 +58,7 @@ struct NedfModel {
   __half* wpack = nullptr;
   float* bias_pack = nullptr;
   float* wstream = nullptr;
+  float* wcluster = nullptr;
   int device = 0;
 };
 
@@ -393,7 +394,7 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
     if ((rc = prof_mark(ctx, st, 0, false))) return rc;
     if (a.use_guard) {
       if ((rc = prof_mark(ctx, st, 1, true))) return rc;
-      LAUNCH(ctx, launch_mlp_fp32_stream(F.gt, F.redo, job, out, ctx->n_sms, 8, st));
+      LAUNCH(ctx, launch_mlp_fp32_cluster(F.gt, F.redo, job, out, ctx->n_sms, st));
       if ((rc = prof_mark(ctx, st, 1, false))) return rc;
     }
     add_counts_kernel<<<1, 32, 0, st>>>(F.ls.count, F.redo.count, F.gt.n_groups, F.fj.stats, a.use_guard);
@@ -658,6 +659,10 @@ int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* 
   auto cleanup = [&]() {
     if (m->wT) cudaFree(m->wT);
     if (m->bias) cudaFree(m->bias);
+    if (m->wpack) cudaFree(m->wpack);
+    if (m->bias_pack) cudaFree(m->bias_pack);
+    if (m->wstream) cudaFree(m->wstream);
+    if (m->wcluster) cudaFree(m->wcluster);
     if (m->dev) cudaFree(m->dev);
     delete m;
   };
@@ -680,6 +685,9 @@ int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* 
     e = fp32_pack_stream(params, info->d_in, F, info->n_blocks, info->n_coarse, info->n_fine, &m->wstream);
     if (e != cudaSuccess) { cleanup(); return fail(NEDF_ERR_CUDA, std::string("fp32 pack: ") + cudaGetErrorString(e)); }
     h.wstream = m->wstream;
+    e = fp32_pack_cluster(params, info->d_in, F, info->n_blocks, info->n_coarse, info->n_fine, &m->wcluster);
+    if (e != cudaSuccess) { cleanup(); return fail(NEDF_ERR_CUDA, std::string("fp32 pack: ") + cudaGetErrorString(e)); }
+    h.wcluster = m->wcluster;
     h.tensor_ok = 1;
   }
   e = cudaMalloc(&m->dev, sizeof(DevModel));
@@ -726,6 +734,7 @@ void nedf_model_free(NedfModel* m) {
   if (m->wpack) cudaFree(m->wpack);
   if (m->bias_pack) cudaFree(m->bias_pack);
   if (m->wstream) cudaFree(m->wstream);
+  if (m->wcluster) cudaFree(m->wcluster);
   if (m->dev) cudaFree(m->dev);
   delete m;
 }

@@ -134,7 +134,7 @@ __device__ __forceinline__ void trace_at(bool on, int idx) {
 }
 // wait, accumulating the cycles spent when tracing
 #ifndef NEDF_TC_SPIN
-#define NEDF_TC_SPIN 1
+#define NEDF_TC_SPIN 0   // 1 = spin on mbarrier.test_wait (measured slower: polling competes for shared memory)
 #endif
 __device__ __forceinline__ void twait(uint64_t* bar, uint32_t ph, bool on, unsigned long long& acc) {
   if (on) {
@@ -231,13 +231,16 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
       __syncwarp();
     } else if (warp == 1) {
       // ------------------------------------------------------------------ MMA issuer
+      // Fully warp-uniform (a lane-dependent branch here moves the loop state out of the uniform
+      // datapath and costs ~40% of the kernel); descriptors are base + slot offsets.
       int stage = 0, es = 0, ti = 0;
       uint32_t phase = 0, ephase = 0;
       uint32_t layer_ctr = 0;
       const uint32_t id256 = tc::idesc_f16(128, 256), id128 = tc::idesc_f16(128, 128);
-      const uint32_t ring_s = tc::smem_u32(ring), enc_s = tc::smem_u32(enc);
+      const uint64_t dring = tc::sw128_desc(tc::smem_u32(ring)), denc = tc::sw128_desc(tc::smem_u32(enc));
+      constexpr uint64_t kSlotDesc = kStageBytes >> 4, kEncDesc = kEncBytes >> 4;
       for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
-        const bool tr = trace_cta && ti == 1 && lane == 0;
+        const bool tr = trace_cta && ti == 1;
         unsigned long long w_full = 0, w_epi = 0, w_enc = 0;
         trace_at(tr, 0);
         // ---- head (SS): A = encoded rays, B = W_head [256 x 64] per sample point
@@ -250,12 +253,11 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           twait(&S.full[stage], phase, tr, w_full);
           twait(&S.full[stage + 1], phase, tr, w_full);
           tc::tc_fence_after();
-          const uint32_t a0 = enc_s + es * kEncBytes, b0 = ring_s + stage * kStageBytes;
+          const uint64_t a0 = denc + es * kEncDesc, b0 = dring + stage * kSlotDesc;
           if (tc::elect_one()) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              tc::mma_ss(tbase + kAccCol, tc::sw128_desc(a0 + k * 32), tc::sw128_desc(b0 + k * 32), id256,
-                         (c | k) ? 1u : 0u);
+              tc::mma_ss(tbase + kAccCol, a0 + 2 * k, b0 + 2 * k, id256, (c | k) ? 1u : 0u);
             tc::mma_commit_mc(&S.empty[stage], cmask);
             tc::mma_commit_mc(&S.empty[stage + 1], cmask);
             tc::mma_commit(&S.enc_empty[es]);
@@ -274,34 +276,27 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
         ++layer_ctr;
         // ---- 32 residual-block layers + the fused tail (TS, two 128-column slices)
         for (int L = 1; L <= kBodyLayers + 1; ++L) {
-          const uint32_t a_col = (L & 1) ? kAPCol : kAQCol;   // fc1 and tail read x, fc2 reads h
+          const uint32_t a_col = tbase + ((L & 1) ? kAPCol : kAQCol);   // fc1 and tail read x, fc2 reads h
           const uint32_t par = (layer_ctr - 1) & 1;
           trace_at(tr, L);
           twait(&S.epi_done[0], par, tr, w_epi);               // acc slice 0 free, A chunks 0-1 ready
-          bool have1 = false;
-#pragma unroll 1
-          for (int s = 0; s < 2; ++s) {
-#pragma unroll 1
-            for (int kc = 0; kc < 4; ++kc) {
-              if (!have1 && (kc >= 2 || s == 1)) {               // acc slice 1 free, A chunks 2-3 ready
-                twait(&S.epi_done[1], par, tr, w_epi);
-                have1 = true;
-              }
-              twait(&S.full[stage], phase, tr, w_full);
-              tc::tc_fence_after();
-              const uint32_t b0 = ring_s + stage * kStageBytes;
-              const uint32_t ac = tbase + a_col + kc * 32;
-              if (tc::elect_one()) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  tc::mma_ts(tbase + kAccCol + 128 * s, ac + k * 8, tc::sw128_desc(b0 + k * 32), id128,
-                             (kc | k) ? 1u : 0u);
-                tc::mma_commit_mc(&S.empty[stage], cmask);
-                if (kc == 3) tc::mma_commit(&S.acc_full[s]);
-              }
-              __syncwarp();
-              if (++stage == kStages) { stage = 0; phase ^= 1; }
+          for (int j = 0; j < 8; ++j) {
+            const int s = j >> 2, kc = j & 3;
+            if (j == 2) twait(&S.epi_done[1], par, tr, w_epi);    // acc slice 1 free, A chunks 2-3 ready
+            twait(&S.full[stage], phase, tr, w_full);
+            tc::tc_fence_after();
+            const uint64_t b0 = dring + stage * kSlotDesc;
+            if (tc::elect_one()) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                tc::mma_ts(tbase + kAccCol + 128 * s, a_col + kc * 32 + k * 8, b0 + 2 * k, id128,
+                           (kc | k) ? 1u : 0u);
+              tc::mma_commit_mc(&S.empty[stage], cmask);
+              if (kc == 3) tc::mma_commit(&S.acc_full[s]);
             }
+            __syncwarp();
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
           trace_at(tr, 40 + L);
           ++layer_ctr;

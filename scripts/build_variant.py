@@ -14,10 +14,12 @@ name, src, *defs = sys.argv[1:]
 B.build()
 out_dir = ROOT / "_exp"
 out_dir.mkdir(exist_ok=True)
-src = B.CSRC / src
+src = Path(src) if Path(src).is_absolute() else B.CSRC / src   # an absolute path replaces csrc/<same stem>.cu
 obj = out_dir / f"{name}_{src.stem}.o"
-subprocess.run([B.nvcc(), *B.ARCH, *B.NVCC_FLAGS, *defs, "-c", str(src), "-o", str(obj)], check=True,
-               capture_output=True)
+r = subprocess.run([B.nvcc(), *B.ARCH, *B.NVCC_FLAGS, *defs, "-c", str(src), "-o", str(obj)],
+                   capture_output=True, text=True)
+if r.returncode != 0:
+    sys.exit(r.stderr)
 objs = [obj if o.stem == src.stem else o for o in sorted(B.OBJDIR.glob("*.o"))]
 subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-o", str(out_dir / f"{name}.so"), *map(str, objs), "-lcudart"],
                check=True)
