@@ -46,6 +46,11 @@ int nedf_diag_tc_trace(int enable, unsigned long long* out, int n);
  * tile cycles. */
 int nedf_diag_tc2_trace(int enable, unsigned long long* out, int n);
 
+/* Timeline of cluster 0 / CTA 0 of the cluster-split fp32 guard kernel (clock64):
+ * per tile i < 4, [64 i] start, [64 i + 1] rays set up, [64 i + 2] features
+ * landed, [64 i + 3 + L] layer L landed, [64 i + 40] decoded; n <= 256. */
+int nedf_diag_cl_trace(int enable, unsigned long long* out, int n);
+
 /* tcgen05 issue-rate probe: `iters` M=128 x N MMAs (ts: A from TMEM) from one
  * warp, committing every `per_commit`; writes elapsed clock64 cycles to out_dev. */
 int nedf_diag_mma_rate(int ts, int n, int iters, int per_commit, unsigned long long* out_dev);

@@ -7,11 +7,20 @@
 // share each ray tile: CTA r owns output columns [32 r, 32 r + 32) of every
 // layer, reads only its 1/8 of the weights (straight from L2, each thread a
 // contiguous 128-byte run per layer), and scatters its outputs into every
-// peer's activation buffer through distributed shared memory; one cluster
-// barrier per layer publishes them.  Same arithmetic as mlp_fp32s.cu: float64
-// features, float32 weights / accumulation (a different summation order).
+// peer's activation buffer with st.async through distributed shared memory.
+// Each store completes transaction bytes on the receiving CTA's mbarrier, so
+// a CTA starts layer L+1 as soon as all 16 KB of layer L have landed -- no
+// cluster-wide barrier (whose release semantics would also drain the weight
+// prefetch) per layer.  Buffer reuse is safe without one: a CTA can only
+// produce layer L+1 after receiving every peer's layer-L outputs, i.e. after
+// every peer finished reading the buffer layer L+1 overwrites.  Two layer
+// barriers alternate so a peer one layer ahead never completes the current
+// phase.  Same arithmetic as mlp_fp32s.cu: float64 features, float32 weights
+// and accumulation (a different summation order).
 //
-// Thread (kp, c): K part kp = warp (K / 8 rows), output column c = lane.
+// Thread layout (256 threads): column quad cg = lane & 7 (columns 4 cg .. 4 cg + 3
+// of the CTA's 32), K part kp = 4 warp + (lane >> 3) of 32 (8 K rows per layer,
+// 32 for the head), so every x value loaded from shared memory feeds 4 FMAs.
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -20,35 +29,55 @@
 #include "encode.cuh"
 #include "frame.cuh"
 #include "tc_ptx.cuh"
+#include "../../include/nedf_b200_diag.h"
 
 namespace nedf {
 namespace {
 
 constexpr int kC = 8;                 // CTAs per cluster
-constexpr int kThreads = 256;         // 8 K parts x 32 columns
+constexpr int kThreads = 256;         // 32 K parts x 8 column quads
+constexpr int kKP = 32;               // K parts
 constexpr int kR = 16;                // rays per cluster tile
 constexpr int kHeadK = 1024;          // 16 points x (63 features + 1 zero)
-constexpr int kHeadPer = kHeadK / 8;  // 128 weights per thread
-constexpr int kBodyPer = 256 / 8;     // 32 weights per thread
+constexpr int kChunk = 32;            // weights per thread per chunk: 8 K rows x 4 columns
+constexpr int kHeadChunks = kHeadK / kKP / 8;   // 4
 constexpr int kLayers = 34;           // head, 32 block layers, fused tail
-constexpr size_t kHeadFloats = (size_t)kC * kThreads * kHeadPer;   // 262144
-constexpr size_t kLayerFloats = (size_t)kC * kThreads * kBodyPer;  // 65536
+constexpr int kChunks = kHeadChunks + kLayers - 1;                   // 37
+constexpr size_t kHeadFloats = (size_t)kC * kThreads * kHeadChunks * kChunk;   // 262144
+constexpr size_t kLayerFloats = (size_t)kC * kThreads * kChunk;                // 65536
 
 struct ClSmem {
   float f[kR][kHeadK];
   float x[kR][256];
   float h[kR][256];
-  float part[8][kR][32];
+  float part[kKP / 4][kR][32];   // per warp (4 K parts, pre-reduced by shuffle)
   double ray[kR][8];
   uint32_t pix[kR], obj[kR];
   int valid[kR];
+  uint64_t feat_bar;             // features of the tile: 64 KB from the 8 CTAs
+  uint64_t layer_bar[2];         // layer L outputs (16 KB from the 8 CTAs) on layer_bar[L & 1]
 };
+constexpr uint32_t kFeatBytes = kR * kHeadK * 4;
+constexpr uint32_t kLayerBytes = kR * 256 * 4;
 
-__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+// remote store that completes its bytes on the receiving CTA's mbarrier
+__device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "f"(a), "f"(b), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_f32(uint32_t addr, float v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(addr), "f"(v),
+               "r"(mbar)
+               : "memory");
 }
 
 }  // namespace
+
+// optional timeline of cluster 0 / CTA 0 (diagnostics, nedf_diag_cl_trace): per tile i < 4,
+// [64 i + 0] start, [+1] rays set up, [+2] features landed, [+3 + L] layer L landed, [+40] decoded
+__device__ unsigned long long g_cl_trace[256];
+__device__ int g_cl_trace_on;
 
 __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
 mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
@@ -56,7 +85,8 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
   ClSmem& S = *reinterpret_cast<ClSmem*>(smem_raw);
   __shared__ int s_tiles[65];
   const int tid = threadIdx.x;
-  const int kp = tid >> 5, c = tid & 31;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int cg = lane & 7, kp = 4 * warp + (lane >> 3);
   const uint32_t rank = tc::cluster_rank();
   const int cid = blockIdx.x / kC, n_cl = gridDim.x / kC;
   const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
@@ -75,10 +105,18 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       cum += (ls.count[g] + kR - 1) / kR;
       s_tiles[g + 1] = cum;
     }
+    tc::mbar_init(&S.feat_bar, 1);
+    tc::mbar_init(&S.layer_bar[0], 1);
+    tc::mbar_init(&S.layer_bar[1], 1);
+    tc::mbar_fence_init();
   }
-  __syncthreads();
+  tc::cluster_sync();           // peers' barriers initialised before anyone stores into them
   const int total = s_tiles[ng];
-  for (int t = cid; t < total; t += n_cl) {
+  uint32_t feat_phase = 0, layer_count = 0;
+  int ti = 0;
+  for (int t = cid; t < total; t += n_cl, ++ti) {
+    const bool tr = g_cl_trace_on && cid == 0 && rank == 0 && tid == 0 && ti < 4;
+    if (tr) g_cl_trace[64 * ti] = clock64();
     int g = 0;
     while (g < ng - 1 && t >= s_tiles[g + 1]) ++g;
     const int lt = t - s_tiles[g];
@@ -105,6 +143,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       }
     }
     __syncthreads();
+    if (tr) g_cl_trace[64 * ti + 1] = clock64();
     // ---- head features: this CTA computes sample points 2 rank, 2 rank + 1 and broadcasts them
     // (float64, geometry.py:312-342); one (ray, point, coordinate, level) per thread
     for (int e = tid; e < kR * 2 * 33; e += kThreads) {
@@ -122,7 +161,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
           const double p = ((S.ray[r][a] + tt * S.ray[r][3 + a]) - m.c[a]) / m.h[a];
           if (lev < 10) {
             double sn, cs;
-            sincos(p * ldexp(3.141592653589793, lev), &sn, &cs);
+            sincospi(ldexp(p, lev), &sn, &cs);     // sin/cos(2^lev pi p), exact argument scaling
             v0 = (float)sn;
             v1 = (float)cs;
           } else {
@@ -133,59 +172,125 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       float* dst = &S.f[r][64 * pt + 21 * a];
 #pragma unroll
       for (int q = 0; q < kC; ++q) {
+        const uint32_t fb = remote(q, &S.feat_bar);
         if (lev < 10) {
-          st_cluster_f32(remote(q, dst + 1 + 2 * lev), v0);
-          st_cluster_f32(remote(q, dst + 2 + 2 * lev), v1);
+          st_async_f32(remote(q, dst + 1 + 2 * lev), v0, fb);     // odd offsets for a = 0: no v2
+          st_async_f32(remote(q, dst + 2 + 2 * lev), v1, fb);
         } else {
-          st_cluster_f32(remote(q, dst), v0);
-          if (a == 0) st_cluster_f32(remote(q, &S.f[r][64 * pt + 63]), 0.f);
+          st_async_f32(remote(q, dst), v0, fb);
+          if (a == 0) st_async_f32(remote(q, &S.f[r][64 * pt + 63]), 0.f, fb);
         }
       }
     }
-    tc::cluster_sync();
+    if (tid == 0) tc::mbar_expect_tx(&S.feat_bar, kFeatBytes);
+    tc::mbar_wait(&S.feat_bar, feat_phase);
+    feat_phase ^= 1;
+    if (tr) g_cl_trace[64 * ti + 2] = clock64();
     // ---- 34 layers: head (K = 1024), 16 x (fc1, fc2), fused tail (nn.py:115-135)
+    // The thread's weights stream as 37 chunks of 16 floats (head 4, then one per layer); the
+    // next chunk is loaded into registers while the current one is multiplied, so L2 latency
+    // overlaps the FMAs and the exchange.
     const float* wl = m.wcluster;
+    const float* bias_p = m.bias_pack;
+    auto chunk_ptr = [&](int q) -> const float4* {
+      const size_t t = (size_t)rank * kThreads + tid;
+      const float* p = q < kHeadChunks ? wl + (t * kHeadChunks + q) * kChunk
+                                       : wl + kHeadFloats + (size_t)(q - kHeadChunks) * kLayerFloats + t * kChunk;
+      return reinterpret_cast<const float4*>(p);
+    };
+    float4 wcur[8], wnxt[8];
+    {
+      const float4* p = chunk_ptr(0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) wcur[i] = __ldg(p + i);
+    }
+    const int rr = tid >> 4, cc2 = 2 * (tid & 15), col2 = 32 * (int)rank + cc2;   // reduce role
+    float2 bnext = __ldg(reinterpret_cast<const float2*>(bias_p + col2));
+    int q = 0;
     for (int L = 0; L < kLayers; ++L) {
-      const int per = L == 0 ? kHeadPer : kBodyPer;
+      const int nch = L == 0 ? kHeadChunks : 1;
       const float* in = L == 0 ? &S.f[0][0] : ((L & 1) ? &S.x[0][0] : &S.h[0][0]);
       const int ld_in = L == 0 ? kHeadK : 256;
-      const float* w = wl + (L == 0 ? 0 : kHeadFloats + (size_t)(L - 1) * kLayerFloats) +
-                       ((size_t)rank * kThreads + tid) * per;
-      float acc[kR];
+      const float2 b = bnext;
+      if (L + 1 < kLayers) bnext = __ldg(reinterpret_cast<const float2*>(bias_p + (L + 1) * 256 + col2));
+      float a[kR][4];
 #pragma unroll
-      for (int r = 0; r < kR; ++r) acc[r] = 0.f;
-      const float* inp = in + kp * per;
-#pragma unroll 2
-      for (int k = 0; k < per; k += 4) {
-        const float4 wv = __ldg(reinterpret_cast<const float4*>(w + k));
+      for (int r = 0; r < kR; ++r) a[r][0] = a[r][1] = a[r][2] = a[r][3] = 0.f;
+      // chunks alternate between two register buffers (no copy, which would wait on the prefetch)
+      auto run_chunk = [&](int j, float4 (&wc)[8], float4 (&wn)[8]) {
+        if (q + 1 < kChunks) {
+          const float4* p = chunk_ptr(q + 1);
 #pragma unroll
-        for (int r = 0; r < kR; ++r) {
-          const float4 a4 = *reinterpret_cast<const float4*>(inp + r * ld_in + k);
-          acc[r] = fmaf(a4.x, wv.x, acc[r]);
-          acc[r] = fmaf(a4.y, wv.y, acc[r]);
-          acc[r] = fmaf(a4.z, wv.z, acc[r]);
-          acc[r] = fmaf(a4.w, wv.w, acc[r]);
+          for (int i = 0; i < 8; ++i) wn[i] = __ldg(p + i);
         }
-      }
+        // this chunk's 8 K rows; float4 i = W[c0 .. c0 + 3][k0 + i]
+        const float* inp = in + kp * (8 * nch) + 8 * j;
 #pragma unroll
-      for (int r = 0; r < kR; ++r) S.part[kp][r][c] = acc[r];
+        for (int h2 = 0; h2 < 2; ++h2) {
+#pragma unroll
+          for (int r = 0; r < kR; ++r) {
+            const float4 x4 = *reinterpret_cast<const float4*>(inp + r * ld_in + 4 * h2);
+            const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float4 w = wc[4 * h2 + e];
+              a[r][0] = fmaf(xs[e], w.x, a[r][0]);
+              a[r][1] = fmaf(xs[e], w.y, a[r][1]);
+              a[r][2] = fmaf(xs[e], w.z, a[r][2]);
+              a[r][3] = fmaf(xs[e], w.w, a[r][3]);
+            }
+          }
+        }
+        ++q;
+      };
+      for (int j = 0; j < nch; ++j) {
+        if (q & 1) run_chunk(j, wnxt, wcur);
+        else run_chunk(j, wcur, wnxt);
+      }
+      if (tr && L == 5) g_cl_trace[64 * ti + 41] = clock64();
+      if (g_cl_trace_on && cid == 0 && rank == 0 && lane == 0 && ti == 0 && L == 5) g_cl_trace[200 + warp] = clock64();
+      // pre-reduce the warp's four K parts (lanes l, l + 8, l + 16, l + 24), then across the 8 warps
+#pragma unroll
+      for (int r = 0; r < kR; ++r)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a[r][u] += __shfl_xor_sync(0xffffffffu, a[r][u], 8);
+          a[r][u] += __shfl_xor_sync(0xffffffffu, a[r][u], 16);
+        }
+      if (lane < 8) {
+#pragma unroll
+        for (int r = 0; r < kR; ++r)
+          *reinterpret_cast<float4*>(&S.part[warp][r][4 * cg]) = make_float4(a[r][0], a[r][1], a[r][2], a[r][3]);
+      }
       __syncthreads();
-      for (int o = tid; o < kR * 32; o += kThreads) {
-        const int r = o >> 5, cc = o & 31, col = 32 * (int)rank + cc;
-        float s = 0.f;
+      if (tr && L == 5) g_cl_trace[64 * ti + 42] = clock64();
+      {   // two adjacent outputs per thread: 16 rays x 32 columns
+        float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s += S.part[q][r][cc];
-        const float b = __ldg(m.bias_pack + L * 256 + col);
-        float v;
+        for (int w = 0; w < kKP / 4; ++w) {
+          const float2 pv = *reinterpret_cast<const float2*>(&S.part[w][rr][cc2]);
+          s0 += pv.x;
+          s1 += pv.y;
+        }
+        float v0, v1;
         float* dst;
-        if (L == 0) { v = s + b; dst = &S.x[r][col]; }                          // head: no activation
-        else if (L == kLayers - 1) { v = s + b; dst = &S.h[r][col]; }            // tail logits
-        else if (L & 1) { v = fmaxf(s + b, 0.f); dst = &S.h[r][col]; }           // fc1
-        else { v = S.x[r][col] + fmaxf(s + b, 0.f); dst = &S.x[r][col]; }        // fc2 + residual
+        if (L == 0) { v0 = s0 + b.x; v1 = s1 + b.y; dst = &S.x[rr][col2]; }                     // head
+        else if (L == kLayers - 1) { v0 = s0 + b.x; v1 = s1 + b.y; dst = &S.h[rr][col2]; }       // tail logits
+        else if (L & 1) { v0 = fmaxf(s0 + b.x, 0.f); v1 = fmaxf(s1 + b.y, 0.f); dst = &S.h[rr][col2]; }   // fc1
+        else {                                                                                 // fc2 + residual
+          v0 = S.x[rr][col2] + fmaxf(s0 + b.x, 0.f);
+          v1 = S.x[rr][col2 + 1] + fmaxf(s1 + b.y, 0.f);
+          dst = &S.x[rr][col2];
+        }
+        const int lb = layer_count & 1;
 #pragma unroll
-        for (int q = 0; q < kC; ++q) st_cluster_f32(remote(q, dst), v);
+        for (int qq = 0; qq < kC; ++qq) st_async_v2(remote(qq, dst), v0, v1, remote(qq, &S.layer_bar[lb]));
       }
-      tc::cluster_sync();
+      if (tr && L == 5) g_cl_trace[64 * ti + 43] = clock64();
+      if (tid == 0) tc::mbar_expect_tx(&S.layer_bar[layer_count & 1], kLayerBytes);
+      tc::mbar_wait(&S.layer_bar[layer_count & 1], (layer_count >> 1) & 1);
+      ++layer_count;
+      if (tr) g_cl_trace[64 * ti + 3 + L] = clock64();
     }
     // ---- decode: fine = logits[0:128), coarse = [128:192), alpha = [192] (model.py:277-293)
     if (rank == 0 && tid < kR && S.valid[tid]) {
@@ -208,8 +313,27 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       }
     }
     __syncthreads();
+    if (tr) g_cl_trace[64 * ti + 40] = clock64();
   }
+  tc::cluster_sync();           // no CTA leaves while its stores to peers may be in flight
 }
+
+}  // namespace nedf
+
+extern "C" int nedf_diag_cl_trace(int enable, unsigned long long* out, int n) {
+  using namespace nedf;
+  if (enable >= 0) {
+    int v = enable;
+    if (cudaMemcpyToSymbol(g_cl_trace_on, &v, sizeof(int)) != cudaSuccess) return NEDF_ERR_CUDA;
+  }
+  if (out && n > 0) {
+    if (n > 256) n = 256;
+    if (cudaMemcpyFromSymbol(out, g_cl_trace, n * sizeof(unsigned long long)) != cudaSuccess) return NEDF_ERR_CUDA;
+  }
+  return NEDF_OK;
+}
+
+namespace nedf {
 
 cudaError_t launch_mlp_fp32_cluster(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
                                     int n_sms, cudaStream_t stream) {
@@ -233,8 +357,10 @@ cudaError_t launch_mlp_fp32_cluster(const GroupTable& gt, const ListSet& ls, con
   return cudaGetLastError();
 }
 
-// Cluster image: layer L, CTA r, thread (kp, c) -> `per` consecutive floats
-// W[out = 32 r + c][in = kp * per + k], k < per (head rows are the 16 points'
+// Cluster image: layer L, CTA r, thread t (column quad cg = t & 7, K part
+// kp = 4 (t >> 5) + ((t >> 3) & 3)), chunk j -> 32 floats: float4 i =
+// W[c0 .. c0 + 3][k] for K row k = kp * 8 n + 8 j + i (n = chunks of the layer:
+// 4 for the head, 1 after) and c0 = 32 r + 4 cg (head rows are the 16 points'
 // 63 features + 1 zero; tail outputs: fine 0-127, coarse 128-191, alpha 192).
 cudaError_t fp32_pack_cluster(const float* P, int d_in, int F, int n_blocks, int n_coarse, int n_fine, float** dev) {
   if (F != 256 || n_blocks != 16 || d_in != kDin || n_coarse != 64 || n_fine != 128) return cudaErrorInvalidValue;
@@ -256,12 +382,19 @@ cudaError_t fp32_pack_cluster(const float* P, int d_in, int F, int n_blocks, int
     return 0.f;
   };
   for (int L = 0; L < kLayers; ++L) {
-    const int per = L == 0 ? kHeadPer : kBodyPer;
-    float* dst = img.data() + (L == 0 ? 0 : kHeadFloats + (size_t)(L - 1) * kLayerFloats);
+    const int nch = L == 0 ? kHeadChunks : 1;
+    float* base = img.data() + (L == 0 ? 0 : kHeadFloats + (size_t)(L - 1) * kLayerFloats);
     for (int r = 0; r < kC; ++r)
       for (int t = 0; t < kThreads; ++t) {
-        const int kp = t >> 5, cc = t & 31, o = 32 * r + cc;
-        for (int k = 0; k < per; ++k) dst[((size_t)r * kThreads + t) * per + k] = w_of(L, o, kp * per + k);
+        const int cg = t & 7, kp = 4 * (t >> 5) + ((t >> 3) & 3);
+        const int c0 = 32 * r + 4 * cg;
+        for (int j = 0; j < nch; ++j) {
+          float* dst = base + (((size_t)r * kThreads + t) * nch + j) * kChunk;
+          for (int i = 0; i < 8; ++i) {
+            const int k = kp * 8 * nch + 8 * j + i;
+            for (int u = 0; u < 4; ++u) dst[4 * i + u] = w_of(L, c0 + u, k);
+          }
+        }
       }
   }
   cudaError_t e = cudaMalloc(dev, img.size() * sizeof(float));
