@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
   const ListSet& ls = a.ls;
   const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
   const bool trace_cta = g_tc_trace_on && blockIdx.x == 0;
+  const int trace_tile = g_tc_trace_on;   // nedf_diag_tc_trace(k): timeline of tile k
   const uint32_t rank = csize > 1 ? tc::cluster_rank() : 0;
   const int cid = blockIdx.x / csize, n_cl = gridDim.x / csize;
   const uint16_t cmask = (uint16_t)((1u << csize) - 1);
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
         uint32_t phase = 0;
         int ti = 0;
         for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
-          const bool tr = trace_cta && ti == 1 && lane == 0;
+          const bool tr = trace_cta && ti == trace_tile && lane == 0;
           int g, n;
           int64_t base;
           tile_lookup(S.tiles, ng, t, ls, csize, rank, g, base, n);
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
       const uint64_t dring = tc::sw128_desc(tc::smem_u32(ring)), denc = tc::sw128_desc(tc::smem_u32(enc));
       constexpr uint64_t kSlotDesc = kStageBytes >> 4, kEncDesc = kEncBytes >> 4;
       for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
-        const bool tr = trace_cta && ti == 1;
+        const bool tr = trace_cta && ti == trace_tile;
         unsigned long long w_full = 0, w_epi = 0, w_enc = 0;
         trace_at(tr, 0);
         // ---- head (SS): A = encoded rays, B = W_head [256 x 64] per sample point
@@ -248,8 +249,10 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           tc::mbar_wait(&S.epi_done[0], (layer_ctr - 1) & 1);
           tc::mbar_wait(&S.epi_done[1], (layer_ctr - 1) & 1);
         }
+        trace_at(tr, 80);
         for (int c = 0; c < 16; ++c) {
           twait(&S.enc_full[es], ephase, tr, w_enc);
+          trace_at(tr, 81 + c);
           twait(&S.full[stage], phase, tr, w_full);
           twait(&S.full[stage + 1], phase, tr, w_full);
           tc::tc_fence_after();
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
     int es = 0, ti = 0;
     uint32_t ephase = 0;
     for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
-      const bool tr = trace_cta && ti == 1 && tid == 128;
+      const bool tr = trace_cta && ti == trace_tile && tid == 128;
       int g, n;
       int64_t base;
       tile_lookup(S.tiles, ng, t, ls, csize, rank, g, base, n);
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
     float x[2][2][32];                      // [slice][32-column chunk][column]
     int ti = 0;
     for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
-      const bool tr = trace_cta && ti == 1 && tid == 256;
+      const bool tr = trace_cta && ti == trace_tile && tid == 256;
       int g, n;
       int64_t base;
       tile_lookup(S.tiles, ng, t, ls, csize, rank, g, base, n);
@@ -503,17 +506,17 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
         tc::mbar_wait(&S.acc_full[s], layer_ctr & 1);
         tc::tc_fence_after();
         trace_at(tr, 100 + 33 * 8 + s);
+        uint32_t vv2[2][32];               // both 32-column parts loaded, then the slice is released
+        tc::tmem_ld32(lane_addr + kAccCol + 128 * s + 64 * hc, vv2[0]);
+        tc::tmem_ld32(lane_addr + kAccCol + 128 * s + 64 * hc + 32, vv2[1]);
+        tc::tmem_ld_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.epi_done[s]);
 #pragma unroll
         for (int j2 = 0; j2 < 2; ++j2) {
           const int col = 128 * s + 64 * hc + 32 * j2;
-          uint32_t v[32];
-          tc::tmem_ld32(lane_addr + kAccCol + col, v);
-          tc::tmem_ld_wait();
-          if (j2 == 1) {                   // accumulator slice fully read: release it
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&S.epi_done[s]);
-          }
+          const uint32_t* v = vv2[j2];
           if (s == 1 && hc == 1) {         // alpha logit at tail column 192, then padding
             if (j2 == 0) {
               alpha = __uint_as_float(v[0]) + bt[192];

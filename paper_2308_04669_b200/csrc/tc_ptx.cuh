@@ -3,6 +3,7 @@
 // instruction descriptors.  Compiled only for sm_100a.
 #pragma once
 
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -39,10 +40,22 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifdef NEDF_TC_WATCHDOG
+// debug builds: report and trap on a wait that never completes
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  long long n = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++n == (1ll << 24) && (threadIdx.x & 31) == 0)
+      printf("nedf watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n", (int)blockIdx.x,
+             (int)threadIdx.x, smem_u32(bar), parity);
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+#endif
 // non-blocking probe (mbarrier.test_wait): spin without the try_wait suspend window
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;

@@ -23,7 +23,8 @@ scene, cam, lights, cfg = scenes.build(spec)
 buf = pipeline.FrameBuffers(cam.width, cam.height)
 pipeline.nedf_generation_step(scene, cam, buf)
 torch.cuda.synchronize()
-tr(1, None, 0)
+TILE = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+tr(TILE, None, 0)
 pipeline.nedf_generation_step(scene, cam, buf)
 torch.cuda.synchronize()
 out = (C.c_ulonglong * 1024)()
@@ -43,3 +44,4 @@ for L in range(34):
           f"epi ready {ready} done {done}  epi[s3] {done[3] - ready[3] if done[3] and ready[3] else None}")
 print("tile cycles (MMA start L0 -> epi done tail):", rel(104 + 8 * 33 + 3))
 print("MMA waits in this tile: full", int(t[600]), "epi_done", int(t[601]), "enc_full", int(t[602]))
+print("MMA head: epi_done(tail) passed at", rel(80), "; point c ready at", [rel(81 + c) for c in range(16)])
