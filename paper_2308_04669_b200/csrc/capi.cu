@@ -157,6 +157,18 @@ int build_scene(NedfContext* ctx, const NedfObject* objs, int n_objs, const Nedf
       }
       sc.objs_per_group[g] += 1;
       d.group = g;
+      {   // world bounding sphere of the relaxed box: v_world = s R v_local + T
+        const DevModel& hm = o.model->host;
+        double cl[3], r2 = 0;
+        for (int a = 0; a < 3; ++a) {
+          cl[a] = 0.5 * (hm.bmin[a] + hm.bmax[a]);
+          const double h = 0.5 * (hm.bmax[a] - hm.bmin[a]);
+          r2 += h * h;
+        }
+        for (int i = 0; i < 3; ++i)
+          d.bs_c[i] = (float)(o.T[i] + o.s * (o.R[3 * i] * cl[0] + o.R[3 * i + 1] * cl[1] + o.R[3 * i + 2] * cl[2]));
+        d.bs_r = (float)(o.s * std::sqrt(r2));
+      }
       if (!o.model->host.tensor_ok) sc.all_tc = false;
     } else if (o.depth_kind == NEDF_DEPTH_ANALYTIC) {
       if (o.depth_field < 0 || o.depth_field >= n_fields)

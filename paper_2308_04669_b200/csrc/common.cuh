@@ -56,7 +56,24 @@ struct DevObj {
   double sigma_default;             // default_sigma_threshold (pipeline.py:196-199)
   int recompute;                    // STEP 1 with a plane cache: 1 = evaluate this object's plane
   int pad2;
+  float bs_c[3], bs_r;              // NeDF objects: world-space bounding sphere of the relaxed box (fp32 pre-test)
 };
+
+// Conservative fp32 rejection before the float64 slab clip: true only when the
+// ray (o + t d, t >= 0) certainly misses the sphere (centre c, radius r)
+// -- the margin covers fp32 rounding of coordinates up to ~1e4 with room to spare,
+// so the exact clip still decides every pair that could hit.
+__device__ __forceinline__ bool sphere_miss(const DevObj& ob, const double o[3], const double d[3]) {
+  const float wx = ob.bs_c[0] - (float)o[0], wy = ob.bs_c[1] - (float)o[1], wz = ob.bs_c[2] - (float)o[2];
+  const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
+  const float w2 = wx * wx + wy * wy + wz * wz;
+  const float tca = wx * dx + wy * dy + wz * dz;
+  const float r = ob.bs_r * 1.001f + 1e-3f * (1.0f + sqrtf(w2));
+  if (w2 <= r * r) return false;             // origin inside (or near) the sphere: no decision
+  if (tca < 0.f) return true;                // sphere behind the origin
+  const float dd = dx * dx + dy * dy + dz * dz;
+  return w2 - tca * tca / dd > r * r;        // the line passes outside
+}
 
 struct DevCam {
   double pos[3];

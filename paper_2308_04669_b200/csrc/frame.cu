@@ -55,7 +55,7 @@ __global__ void setup_kernel(FrameJob fj, GroupTable gt, ListSet ls, int mode) {
       if (mode == RAY_PRIMARY && fj.planes != nullptr && !ob.recompute) continue;   // cached plane kept
       if (ob.depth_kind == NEDF_DEPTH_NEDF) {
         bool hit = false;
-        if (live) {
+        if (live && !sphere_miss(ob, o, d)) {
           const DevModel& m = gt.models[ob.group];
           double lo[3], ld[3], t0, t1;
           to_local(ob, o, d, lo, ld);
