@@ -40,6 +40,7 @@ struct DevBuf {
     bytes = 0;
     size_t n = std::max<size_t>(need, 256);
     cudaError_t e = cudaMalloc(&ptr, n);
+    if (e == cudaSuccess) e = cudaMemset(ptr, 0, n);     // counters (stats, list counts) start at zero
     if (e == cudaSuccess) bytes = n;
     return e;
   }
@@ -78,6 +79,10 @@ struct NedfContext {
   DevBuf models, objs, fields, rows, offsets, counts, redo_counts, lists_pix, lists_obj, redo_pix, redo_obj,
       key, skey, stats, tile_counter;
   int64_t h2d_bytes = 0;
+  // mapped pinned mirror of the 8 stats counters: read back by a one-warp kernel, so reading stats
+  // never queues behind a caller's large device-to-host copy on the copy engine
+  unsigned long long* stats_host = nullptr;
+  unsigned long long* stats_host_dev = nullptr;
 };
 
 namespace {
@@ -534,6 +539,12 @@ int nedf_context_create(int device, NedfContext** out) {
   NedfContext* c = new NedfContext();
   c->device = device;
   c->n_sms = prop.multiProcessorCount;
+  if (cudaHostAlloc(&c->stats_host, 8 * sizeof(unsigned long long), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&c->stats_host_dev, c->stats_host, 0) != cudaSuccess) {
+    if (c->stats_host) cudaFreeHost(c->stats_host);
+    delete c;
+    return fail(NEDF_ERR_CUDA, "mapped host allocation failed");
+  }
   *out = c;
   return NEDF_OK;
 }
@@ -545,6 +556,7 @@ void nedf_context_destroy(NedfContext* c) {
                     &c->lists_pix, &c->lists_obj, &c->redo_pix, &c->redo_obj, &c->key, &c->skey, &c->stats,
                     &c->tile_counter};
   for (DevBuf* b : bufs) b->release();
+  if (c->stats_host) cudaFreeHost(c->stats_host);
   delete c;
 }
 
@@ -591,9 +603,9 @@ int nedf_read_stats(NedfContext* c, NedfStepStats* out, void* stream) {
   unsigned long long h[8] = {0};
   if (c->stats.ptr) {
     cudaStream_t st = (cudaStream_t)stream;
-    CUDA_TRY(cudaMemcpyAsync(h, c->stats.ptr, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(launch_stats_export(c->stats.as<unsigned long long>(), c->stats_host_dev, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    CUDA_TRY(cudaMemsetAsync(c->stats.ptr, 0, sizeof(h), st));
+    for (int i = 0; i < 8; ++i) h[i] = reinterpret_cast<volatile unsigned long long*>(c->stats_host)[i];
   }
   out->covered = (int64_t)h[0];
   out->resampled = (int64_t)h[1];

@@ -317,6 +317,17 @@ cudaError_t launch_explicit_setup(const RayJob& job, const GroupTable& gt, const
   explicit_setup_kernel<<<grid_for(n, n_sms), 256, 0, st>>>(job, gt, ls, out, n);
   return cudaGetLastError();
 }
+__global__ void stats_export_kernel(unsigned long long* stats, unsigned long long* host_mapped) {
+  const int i = threadIdx.x;
+  if (i < 8) {
+    host_mapped[i] = stats[i];
+    stats[i] = 0;
+  }
+}
+cudaError_t launch_stats_export(unsigned long long* stats, unsigned long long* host_mapped, cudaStream_t st) {
+  stats_export_kernel<<<1, 32, 0, st>>>(stats, host_mapped);
+  return cudaGetLastError();
+}
 cudaError_t launch_iota_setup(const ListSet& ls, int64_t n, int n_sms, cudaStream_t st) {
   iota_setup_kernel<<<grid_for(n, n_sms), 256, 0, st>>>(ls, n);
   return cudaGetLastError();

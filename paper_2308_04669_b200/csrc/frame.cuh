@@ -67,6 +67,8 @@ struct TcArgs {
   int use_guard;
   int* tile_counter;
 };
+// copy the 8 frame counters to mapped host memory and clear them (nedf_read_stats)
+cudaError_t launch_stats_export(unsigned long long* stats, unsigned long long* host_mapped, cudaStream_t st);
 bool tc_available();
 // csize = CTAs per cluster sharing one multicast weight stream (1, 2 or 4)
 cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, int csize, cudaStream_t stream);
