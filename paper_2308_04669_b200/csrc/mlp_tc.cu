@@ -40,8 +40,7 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kStageBytes = 16384;         // [128 N x 64 K] fp16, 128B swizzle
 constexpr int kStages = 8;
-constexpr int kEncStages = 2;
-constexpr int kEncBytes = 16384;           // [128 rows x 64 K] fp16
+constexpr int kEncSlots = 4;               // encoded head A tiles live in TMEM (A_Q columns, 32 per point)
 constexpr int kHeadStages = 32;            // 16 points x [256 N x 64 K] (two stages each)
 constexpr int kLayerStages = 8;            // 2 N slices x 4 K chunks
 constexpr int kBodyLayers = 32;
@@ -58,7 +57,8 @@ struct __align__(16) RowRed {
 
 struct TcShared {
   uint64_t full[kStages], empty[kStages];
-  uint64_t enc_full[kEncStages], enc_empty[kEncStages];
+  uint64_t enc_full[kEncSlots], enc_empty[kEncSlots];
+  uint64_t aq_free;              // layer 32's MMAs (last readers of A_Q) completed: the next head may write A_Q
   uint64_t acc_full[2], epi_done[2];
   uint32_t tmem_base;
   int tiles[65];
@@ -66,7 +66,7 @@ struct TcShared {
 };
 
 constexpr size_t kSmemBytes =
-    1024 /*align slack*/ + kStages * kStageBytes + kEncStages * kEncBytes + kBiasBytes + sizeof(TcShared);
+    1024 /*align slack*/ + kStages * kStageBytes + kBiasBytes + sizeof(TcShared);
 
 // cluster tile t = (128 * csize) rays of one group; this CTA (cluster rank r) takes rows [128 r, 128 r + 128)
 __device__ __forceinline__ void tile_lookup(const int* tiles, int ng, int t, const ListSet& ls, int csize,
@@ -157,9 +157,8 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
   // keeps the shared address space and emits LDS/STS instead of generic loads/stores
   unsigned char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* ring = smem;
-  unsigned char* enc = ring + kStages * kStageBytes;
-  float* bias_s = reinterpret_cast<float*>(enc + kEncStages * kEncBytes);
-  TcShared& S = *reinterpret_cast<TcShared*>(enc + kEncStages * kEncBytes + kBiasBytes);
+  float* bias_s = reinterpret_cast<float*>(ring + kStages * kStageBytes);
+  TcShared& S = *reinterpret_cast<TcShared*>(ring + kStages * kStageBytes + kBiasBytes);
 
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);    // warp-uniform role index
@@ -180,7 +179,8 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
       S.tiles[g + 1] = cum;
     }
     for (int i = 0; i < kStages; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], csize); }
-    for (int i = 0; i < kEncStages; ++i) { tc::mbar_init(&S.enc_full[i], 4); tc::mbar_init(&S.enc_empty[i], 1); }
+    for (int i = 0; i < kEncSlots; ++i) { tc::mbar_init(&S.enc_full[i], 4); tc::mbar_init(&S.enc_empty[i], 1); }
+    tc::mbar_init(&S.aq_free, 1);
     for (int i = 0; i < 2; ++i) { tc::mbar_init(&S.acc_full[i], 1); tc::mbar_init(&S.epi_done[i], 8); }
     tc::mbar_fence_init();
   }
@@ -234,12 +234,12 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
       // ------------------------------------------------------------------ MMA issuer
       // Fully warp-uniform (a lane-dependent branch here moves the loop state out of the uniform
       // datapath and costs ~40% of the kernel); descriptors are base + slot offsets.
-      int stage = 0, es = 0, ti = 0;
-      uint32_t phase = 0, ephase = 0;
+      int stage = 0, ti = 0;
+      uint32_t phase = 0;
       uint32_t layer_ctr = 0;
       const uint32_t id256 = tc::idesc_f16(128, 256), id128 = tc::idesc_f16(128, 128);
-      const uint64_t dring = tc::sw128_desc(tc::smem_u32(ring)), denc = tc::sw128_desc(tc::smem_u32(enc));
-      constexpr uint64_t kSlotDesc = kStageBytes >> 4, kEncDesc = kEncBytes >> 4;
+      const uint64_t dring = tc::sw128_desc(tc::smem_u32(ring));
+      constexpr uint64_t kSlotDesc = kStageBytes >> 4;
       for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
         const bool tr = trace_cta && ti == trace_tile;
         unsigned long long w_full = 0, w_epi = 0, w_enc = 0;
@@ -251,24 +251,24 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
         }
         trace_at(tr, 80);
         for (int c = 0; c < 16; ++c) {
-          twait(&S.enc_full[es], ephase, tr, w_enc);
+          const int slot = c & (kEncSlots - 1);              // 4 uses per slot per tile
+          twait(&S.enc_full[slot], (c >> 2) & 1, tr, w_enc);
           trace_at(tr, 81 + c);
           twait(&S.full[stage], phase, tr, w_full);
           twait(&S.full[stage + 1], phase, tr, w_full);
           tc::tc_fence_after();
-          const uint64_t a0 = denc + es * kEncDesc, b0 = dring + stage * kSlotDesc;
+          const uint32_t a0 = tbase + kAQCol + 32 * slot;   // TS: encoded point in TMEM
+          const uint64_t b0 = dring + stage * kSlotDesc;
           if (tc::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc::mma_ss(tbase + kAccCol, a0 + 2 * k, b0 + 2 * k, id256, (c | k) ? 1u : 0u);
+            for (int k = 0; k < 4; ++k) tc::mma_ts(tbase + kAccCol, a0 + 8 * k, b0 + 2 * k, id256, (c | k) ? 1u : 0u);
             tc::mma_commit_mc(&S.empty[stage], cmask);
             tc::mma_commit_mc(&S.empty[stage + 1], cmask);
-            tc::mma_commit(&S.enc_empty[es]);
+            tc::mma_commit(&S.enc_empty[slot]);
           }
           __syncwarp();
           stage += 2;
           if (stage == kStages) { stage = 0; phase ^= 1; }
-          if (++es == kEncStages) { es = 0; ephase ^= 1; }
         }
         if (tc::elect_one()) {
           tc::mma_commit(&S.acc_full[0]);
@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
         }
         __syncwarp();
         trace_at(tr, 40);
+        if (tr) g_tc_trace[603] = w_full;        // weight waits during the head alone
         ++layer_ctr;
         // ---- 32 residual-block layers + the fused tail (TS, two 128-column slices)
         for (int L = 1; L <= kBodyLayers + 1; ++L) {
@@ -301,6 +302,8 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
             __syncwarp();
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
+          if (L == kBodyLayers && tc::elect_one()) tc::mma_commit(&S.aq_free);   // last A_Q reader issued
+          __syncwarp();
           trace_at(tr, 40 + L);
           ++layer_ctr;
         }
@@ -315,8 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
     tc::reg_dealloc<104>();
     // -------------------------------------------------------------------- encoders
     const int row = tid - 128;
-    int es = 0, ti = 0;
-    uint32_t ephase = 0;
+    int ti = 0;
     for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
       const bool tr = trace_cta && ti == trace_tile && tid == 128;
       int g, n;
@@ -355,18 +357,24 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
 #pragma unroll
           for (int j = 0; j < 32; ++j) packed[j] = 0u;
         }
-        tc::mbar_wait(&S.enc_empty[es], ephase ^ 1);
+        // A_Q is free for this tile's points once the previous tile's layer 32 completed; within the
+        // tile, slot pt & 3 is free once point pt - 4 was consumed
+        if (pt == 0 && ti > 0) tc::mbar_wait(&S.aq_free, (ti - 1) & 1);
+        if (pt >= kEncSlots) tc::mbar_wait(&S.enc_empty[pt & 3], ((pt >> 2) - 1) & 1);
         trace_at(tr, 420 + pt);
-        unsigned char* dst = enc + es * kEncBytes;
+        {
+          const uint32_t taddr = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + kAQCol + 32 * (pt & 3);
+          uint32_t lo[16], hi[16];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          *reinterpret_cast<uint4*>(dst + tc::sw128_offset(row, j)) =
-              make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
-        tc::fence_proxy_async_smem();
+          for (int j = 0; j < 16; ++j) { lo[j] = packed[j]; hi[j] = packed[16 + j]; }
+          tc::tmem_st16(taddr, lo);
+          tc::tmem_st16(taddr + 16, hi);
+          tc::tmem_st_wait();
+        }
+        tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&S.enc_full[es]);
+        if (lane == 0) tc::mbar_arrive(&S.enc_full[pt & 3]);
         trace_at(tr, 400 + pt);
-        if (++es == kEncStages) { es = 0; ephase ^= 1; }
       }
     }
   } else {

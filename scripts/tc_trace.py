@@ -43,5 +43,5 @@ for L in range(34):
     print(f"L{L:2d} mma {ms}..{me} (issue {me - ms if ms is not None and me is not None else None})  "
           f"epi ready {ready} done {done}  epi[s3] {done[3] - ready[3] if done[3] and ready[3] else None}")
 print("tile cycles (MMA start L0 -> epi done tail):", rel(104 + 8 * 33 + 3))
-print("MMA waits in this tile: full", int(t[600]), "epi_done", int(t[601]), "enc_full", int(t[602]))
+print("MMA waits in this tile: full", int(t[600]), "(head", int(t[603]), ") epi_done", int(t[601]), "enc_full", int(t[602]))
 print("MMA head: epi_done(tail) passed at", rel(80), "; point c ready at", [rel(81 + c) for c in range(16)])
