@@ -39,7 +39,7 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kStageBytes = 16384;         // [128 N x 64 K] fp16, 128B swizzle
-constexpr int kStages = 8;
+constexpr int kStages = 10;                // even: a head point's two stages sit in adjacent slots
 constexpr int kEncSlots = 4;               // encoded head A tiles live in TMEM (A_Q columns, 32 per point)
 constexpr int kHeadStages = 32;            // 16 points x [256 N x 64 K] (two stages each)
 constexpr int kLayerStages = 8;            // 2 N slices x 4 K chunks
@@ -200,10 +200,11 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
       // congruent to it: bulk copies issued by one thread serialise (~576
       // cycles each, scripts/bulk_rate.py), so one issuer per slot keeps
       // kStages copies in flight.
-      static_assert(kStagesPerTile % kStages == 0, "slots must map to fixed stage residues");
+      static_assert(kStages % 2 == 0 && kStagesPerTile % 2 == 0, "head stage pairs must not wrap");
       if (lane < kStages) {
+        // lane j streams the stages u = j (mod kStages) of the global sequence (296 per tile)
         const int slot = lane;
-        uint32_t phase = 0;
+        uint32_t phase = 0, gbase = 0;
         int ti = 0;
         for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
           const bool tr = trace_cta && ti == trace_tile && lane == 0;
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           int64_t base;
           tile_lookup(S.tiles, ng, t, ls, csize, rank, g, base, n);
           const unsigned char* w = reinterpret_cast<const unsigned char*>(a.gt.models[g].wpack);
-          for (int i = slot; i < kStagesPerTile; i += kStages) {
+          for (int i = (slot - (int)(gbase % kStages) + kStages) % kStages; i < kStagesPerTile; i += kStages) {
             if (NEDF_TC_SPIN) tc::mbar_spin(&S.empty[slot], phase ^ 1);
             else tc::mbar_wait(&S.empty[slot], phase ^ 1);
             if (i == 0) trace_at(tr, 450);
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
             }
             phase ^= 1;
           }
+          gbase += kStagesPerTile;
         }
       }
       __syncwarp();
