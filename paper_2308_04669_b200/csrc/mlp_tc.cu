@@ -213,8 +213,9 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           tile_lookup(S.tiles, ng, t, ls, csize, rank, g, base, n);
           const unsigned char* w = reinterpret_cast<const unsigned char*>(a.gt.models[g].wpack);
           for (int i = (slot - (int)(gbase % kStages) + kStages) % kStages; i < kStagesPerTile; i += kStages) {
-            if (NEDF_TC_SPIN) tc::mbar_spin(&S.empty[slot], phase ^ 1);
-            else tc::mbar_wait(&S.empty[slot], phase ^ 1);
+            // slots 2m, 2m + 1 are released together (one commit per stage pair)
+            if (NEDF_TC_SPIN) tc::mbar_spin(&S.empty[slot & ~1], phase ^ 1);
+            else tc::mbar_wait(&S.empty[slot & ~1], phase ^ 1);
             if (i == 0) trace_at(tr, 450);
             else if (i >= kHeadStages && (i - kHeadStages) % kLayerStages == 0)
               trace_at(tr, 450 + 1 + (i - kHeadStages) / kLayerStages);
@@ -264,8 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           if (tc::elect_one()) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) tc::mma_ts(tbase + kAccCol, a0 + 8 * k, b0 + 2 * k, id256, (c | k) ? 1u : 0u);
-            tc::mma_commit_mc(&S.empty[stage], cmask);
-            tc::mma_commit_mc(&S.empty[stage + 1], cmask);
+            tc::mma_commit_mc(&S.empty[stage], cmask);        // releases slots stage, stage + 1
             tc::mma_commit(&S.enc_empty[slot]);
           }
           __syncwarp();
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
               for (int k = 0; k < 4; ++k)
                 tc::mma_ts(tbase + kAccCol + 128 * s, a_col + kc * 32 + k * 8, b0 + 2 * k, id128,
                            (kc | k) ? 1u : 0u);
-              tc::mma_commit_mc(&S.empty[stage], cmask);
+              if (kc & 1) tc::mma_commit_mc(&S.empty[stage - 1], cmask);   // stage pair done
               if (kc == 3) tc::mma_commit(&S.acc_full[s]);
             }
             __syncwarp();

@@ -186,6 +186,69 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int ts, int N, int ite
         while (clock64() - t0 < (unsigned long long)iters * 74) {
         }
       } else
+      if (per_commit <= -12 && per_commit >= -14) {
+        // -12: per 8 MMAs one wait + fence and one commit; -13: per 8 MMAs two waits and two commits;
+        // -14: per 16 MMAs one wait + fence and one commit
+        __shared__ uint64_t dbar2, cbar2[8];
+        if (tc::elect_one()) {
+          tc::mbar_init(&dbar2, 1);
+          for (int j = 0; j < 8; ++j) tc::mbar_init(&cbar2[j], 1);
+          tc::mbar_fence_init();
+          tc::mbar_arrive(&dbar2);
+        }
+        __syncwarp();
+        const int group = per_commit == -14 ? 16 : 8;
+        t0 = clock64();
+        for (int i = 0; i < iters; i += group) {
+          tc::mbar_wait(&dbar2, 0);
+          if (per_commit == -13) tc::mbar_wait(&dbar2, 0);
+          tc::tc_fence_after();
+          const uint64_t bslot = tc::sw128_desc(tc::smem_u32(smem + 16384));
+          if (tc::elect_one()) {
+            for (int k = 0; k < group; ++k)
+              tc::mma_ts(tbase, tbase + 256 + 8 * (k & 3), bslot + 2 * (k & 3), idesc, 1u);
+            tc::mma_commit(&cbar2[(i / group) & 7]);
+            if (per_commit == -13) tc::mma_commit(&cbar2[((i / group) + 4) & 7]);
+          }
+          __syncwarp();
+        }
+      } else
+      if (per_commit <= -8 && per_commit >= -11 || per_commit == -17 || per_commit == -19 || per_commit == -20) {
+        // variants -8 / -9: the network kernel's per-stage issue pattern -- a (satisfied) mbarrier
+        // wait, tcgen05 fence, elect, 4 MMAs, a commit per stage; -9 also alternates the
+        // accumulator slice every 4 stages and restarts accumulation like the body layers
+        __shared__ uint64_t dbar, cbar[8];
+        if (tc::elect_one()) {
+          tc::mbar_init(&dbar, 1);
+          for (int j = 0; j < 8; ++j) tc::mbar_init(&cbar[j], 1);
+          tc::mbar_fence_init();
+          tc::mbar_arrive(&dbar);
+        }
+        __syncwarp();
+        t0 = clock64();
+        for (int i = 0; i < iters; i += 4) {
+          if (per_commit != -10) {            // -10: commit only
+            if (per_commit == -19) tc::mbar_spin(&dbar, 0);   // -19: mbarrier.test_wait spin
+            else tc::mbar_wait(&dbar, 0);
+            if (per_commit != -17) tc::tc_fence_after();   // -17: wait + commit without the fence
+          }
+          const uint64_t bslot = tc::sw128_desc(tc::smem_u32(smem + 16384)) + (uint64_t)(((i >> 2) & 1) * 1024);
+          const int st = (i >> 2) & 7;
+          const uint32_t dcol = per_commit == -9 ? 128u * ((i >> 4) & 1) : 0u;
+          const bool first = per_commit == -9 && ((i >> 2) & 3) == 0;
+          if (tc::elect_one()) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc::mma_ts(tbase + dcol, tbase + 256 + 8 * k, bslot + 2 * k, idesc, (first && k == 0) ? 0u : 1u);
+            if (per_commit == -20)              // -20: commit with a shared::cta address operand
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"(
+                               (unsigned long long)__cvta_generic_to_shared(&cbar[st]))
+                           : "memory");
+            else if (per_commit != -11) tc::mma_commit(&cbar[st]);   // -11: wait + fence only
+          }
+          __syncwarp();
+        }
+      } else
       for (int i = 0; i < iters; i += 4) {
         if (tc::elect_one()) {
 #pragma unroll

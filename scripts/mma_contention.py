@@ -11,3 +11,11 @@ for ts in (1, 0):
             f(ts, N, 4096, pc, out.data_ptr()); torch.cuda.synchronize()
             f(ts, N, 4096, pc, out.data_ptr()); torch.cuda.synchronize()
             print(f"{'TS' if ts else 'SS'} N={N}: {name:24s} {out[0].item() / 4096:7.1f} cycles/MMA" + (f"  copies {out[1].item()} ({out[1].item() * 16384 / out[0].item():.1f} B/cycle)" if pc <= -5 else ""))
+for pc, name in ((-2, "plain 4-MMA groups"), (-8, "kernel issue pattern"), (-9, "+ slice alternation / restarts"),
+                 (-10, "commit per group only"), (-11, "wait + fence per group only"),
+                 (-12, "per 8 MMAs: 1 wait, 1 commit"), (-13, "per 8 MMAs: 2 waits, 2 commits"),
+                 (-14, "per 16 MMAs: 1 wait, 1 commit"), (-17, "kernel pattern without the fence"),
+                 (-19, "kernel pattern, test_wait spin"), (-20, "kernel pattern, generic commit")):
+    f(1, 128, 4096, pc, out.data_ptr()); torch.cuda.synchronize()
+    out.zero_(); f(1, 128, 4096, pc, out.data_ptr()); torch.cuda.synchronize()
+    print(f"TS N=128: {name:34s} {out[0].item() / 4096:7.1f} cycles/MMA")
