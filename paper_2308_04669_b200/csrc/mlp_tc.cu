@@ -265,8 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           if (tc::elect_one()) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) tc::mma_ts(tbase + kAccCol, a0 + 8 * k, b0 + 2 * k, id256, (c | k) ? 1u : 0u);
-            tc::mma_commit_mc(&S.empty[stage], cmask);        // releases slots stage, stage + 1
-            tc::mma_commit(&S.enc_empty[slot]);
+            tc::mma_commit_mc(&S.empty[stage], cmask);        // releases slots stage, stage + 1 and the point
           }
           __syncwarp();
           stage += 2;
@@ -362,7 +361,11 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
         // A_Q is free for this tile's points once the previous tile's layer 32 completed; within the
         // tile, slot pt & 3 is free once point pt - 4 was consumed
         if (pt == 0 && ti > 0) tc::mbar_wait(&S.aq_free, (ti - 1) & 1);
-        if (pt >= kEncSlots) tc::mbar_wait(&S.enc_empty[pt & 3], ((pt >> 2) - 1) & 1);
+        if (pt >= kEncSlots) {
+          // point pt - 4 consumed: its MMAs are the ones that released its weight-stage pair
+          const uint32_t u = (uint32_t)ti * kStagesPerTile + 2 * (pt - kEncSlots);   // global stage index
+          tc::mbar_wait(&S.empty[u % kStages], (u / kStages) & 1);
+        }
         trace_at(tr, 420 + pt);
         {
           const uint32_t taddr = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + kAQCol + 32 * (pt & 3);
