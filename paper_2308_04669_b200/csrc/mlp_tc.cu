@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
       // ------------------------------------------------------------------ MMA issuer
       // Fully warp-uniform (a lane-dependent branch here moves the loop state out of the uniform
       // datapath and costs ~40% of the kernel); descriptors are base + slot offsets.
-      int stage = 0, ti = 0;
+      int stage = 0, ti = 0, pend = -1;
       uint32_t phase = 0;
       uint32_t layer_ctr = 0;
       const uint32_t id256 = tc::idesc_f16(128, 256), id128 = tc::idesc_f16(128, 128);
@@ -263,11 +263,13 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           const uint32_t a0 = tbase + kAQCol + 32 * slot;   // TS: encoded point in TMEM
           const uint64_t b0 = dring + stage * kSlotDesc;
           if (tc::elect_one()) {
+            if (pend >= 0) tc::mma_commit_mc(&S.empty[pend], cmask);
 #pragma unroll
             for (int k = 0; k < 4; ++k) tc::mma_ts(tbase + kAccCol, a0 + 8 * k, b0 + 2 * k, id256, (c | k) ? 1u : 0u);
             tc::mma_commit_mc(&S.empty[stage], cmask);        // releases slots stage, stage + 1 and the point
           }
           __syncwarp();
+          pend = -1;
           stage += 2;
           if (stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -293,14 +295,17 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
             tc::tc_fence_after();
             const uint64_t b0 = dring + stage * kSlotDesc;
             if (tc::elect_one()) {
+              if (pend >= 0) tc::mma_commit_mc(&S.empty[pend], cmask);   // previous stage pair
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 tc::mma_ts(tbase + kAccCol + 128 * s, a_col + kc * 32 + k * 8, b0 + 2 * k, id128,
                            (kc | k) ? 1u : 0u);
-              if (kc & 1) tc::mma_commit_mc(&S.empty[stage - 1], cmask);   // stage pair done
               if (kc == 3) tc::mma_commit(&S.acc_full[s]);
             }
             __syncwarp();
+            // a stage pair's release is committed right after the NEXT stage's wait, together with
+            // its MMAs: a wait issued right after a commit costs the tensor pipe a bubble
+            pend = (kc & 1) ? stage - 1 : -1;
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
           if (L == kBodyLayers && tc::elect_one()) tc::mma_commit(&S.aq_free);   // last A_Q reader issued
