@@ -245,6 +245,46 @@ int nedf_render_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject*
                       const NedfField* fields, int n_fields, const NedfLight* lights, int n_lights,
                       const NedfRenderConfig* cfg, NedfFrameBuffers* fb, void* stream);
 
+/* ---- output formats (imgio.py): per-pixel conversions on the GPU, so
+ * only 8/16-bit planes or the f32 depth plane are copied to the host for encoding ---- */
+/* (clip(x, 0, 1) * 255 + 0.5) -> uint8, truncating like numpy astype (imgio.py:23-24);
+ * n = element count (3 per pixel for RGB). */
+int nedf_to_u8(const float* src_dev, int64_t n, uint8_t* dst_dev, void* stream);
+/* float64 depth -> float32 NDPT plane, misses stay +inf (imgio.py:63-71). */
+int nedf_depth_to_f32(const double* depth_dev, int64_t n, float* dst_dev, void* stream);
+/* depth_to_gray (imgio.py:88-97): nearest finite surface 255, farthest 0, misses 0;
+ * round half to even like np.round.  scratch_dev: 16 bytes of device memory. */
+int nedf_depth_to_gray(const double* depth_dev, int64_t n, uint8_t* dst_dev, uint64_t* scratch_dev, void* stream);
+/* id plane -> 16-bit grayscale (id + 1, clipped to [0, 65535]; imgio.py:106-111). */
+int nedf_id_to_u16(const int32_t* id_dev, int64_t n, uint16_t* dst_dev, void* stream);
+
+/* ---- GPU distillation (model.py:238-274, nn.py:115-232) ----
+ * A trainer owns fp32 parameters (the .nedm order: head W, b; per block fc1 W, b,
+ * fc2 W, b; tail_a W, b; tail_b W, b), Adam moments and the activation cache for
+ * batches of up to max_batch rays.  Errors: nedf_trainer_last_error(). */
+typedef struct NedfTrainer NedfTrainer;
+const char* nedf_trainer_last_error(void);
+int nedf_trainer_create(int device, const NedfModelInfo* info, const float* params_host, int64_t n_params,
+                        int max_batch, NedfTrainer** out);
+void nedf_trainer_destroy(NedfTrainer* t);
+int nedf_trainer_set_lr(NedfTrainer* t, float lr);
+/* Training batch from host rays in the model frame (build_training_batch, model.py:189-235):
+ * slab clip + encoding, sphere tracing of the analytic oracle field `root`, mu and bin
+ * targets, all on the GPU; hit_host[n] receives the box-hit mask (misses are redrawn
+ * by the caller, as the reference does). */
+int nedf_trainer_batch(NedfTrainer* t, const NedfField* fields, int n_fields, int root, double t_max,
+                       const double* origins_host, const double* dirs_host, int n, uint8_t* hit_host, void* stream);
+/* Explicit batch: features [n][1008], coarse / fine bin targets (-1 = no hit), alpha targets. */
+int nedf_trainer_set_batch(NedfTrainer* t, const float* feats_host, const int32_t* coarse_host,
+                           const int32_t* fine_host, const float* alpha_host, int n, void* stream);
+/* Forward, BCE losses, exact backward into the gradient buffer (loss_and_grads,
+ * model.py:238-248); losses_host[4] = total, coarse, fine, alpha. */
+int nedf_trainer_loss_and_grads(NedfTrainer* t, double* losses_host, void* stream);
+/* Adam with bias correction (nn.py:218-232). */
+int nedf_trainer_adam_step(NedfTrainer* t, void* stream);
+/* Copy the parameters (what = 0) or the last gradients (what = 1) to the host. */
+int nedf_trainer_read(NedfTrainer* t, int what, float* host, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

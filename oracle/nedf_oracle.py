@@ -682,3 +682,153 @@ def quat_to_matrix(q):
         [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
         [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)],
     ])
+
+
+# ---------------------------------------------------------------------------
+# output formats (imgio.py)
+# ---------------------------------------------------------------------------
+
+def to_u8(rgb):
+    """imgio.py:23-24."""
+    return (np.clip(np.asarray(rgb, dtype=np.float64), 0.0, 1.0) * 255.0 + 0.5).astype(np.uint8)
+
+
+def depth_to_gray(depth):
+    """imgio.py:88-97: nearest surface bright, farthest dark, misses black."""
+    depth = np.asarray(depth, dtype=np.float64)
+    finite = np.isfinite(depth)
+    out = np.zeros(depth.shape, dtype=np.uint8)
+    if finite.any():
+        lo, hi = depth[finite].min(), depth[finite].max()
+        span = hi - lo if hi > lo else 1.0
+        out[finite] = np.round((hi - depth[finite]) / span * 255.0).astype(np.uint8)
+    return out
+
+
+def id_to_u16(ids):
+    """imgio.py:106-111 (the values the 16-bit PNG stores)."""
+    return (np.asarray(ids).astype(np.int32) + 1).clip(0, 65535).astype(np.uint16)
+
+
+def depth_raw_bytes(depth, scale=1.0):
+    """imgio.py:63-71: NDPT header + little-endian f32 plane."""
+    import struct
+    depth = np.asarray(depth)
+    h, w = depth.shape
+    return b"NDPT" + struct.pack("<IIf", w, h, scale) + depth.astype("<f4").tobytes(order="C")
+
+
+# ---------------------------------------------------------------------------
+# distillation (model.py:74-81, 189-248; nn.py:115-232) -- float64
+# ---------------------------------------------------------------------------
+
+def segment_batch(mu, half_range, n_coarse=64, n_fine=128):
+    """model.py:74-81."""
+    l = half_range
+    u = (np.clip(mu, -l, l) + l) / (2.0 * l)
+    scaled = u * n_coarse
+    coarse = np.minimum(scaled.astype(int), n_coarse - 1)
+    fine = np.minimum(((scaled - coarse) * n_fine).astype(int), n_fine - 1)
+    return coarse, fine
+
+
+def flat_params(model: "OracleModel"):
+    return [a for w, b in model.weights for a in (w, b)]
+
+
+def forward_cached(model: "OracleModel", feats):
+    """nn.py:115-135 with the activation cache."""
+    W = model.weights
+    x = feats @ W[0][0].T + W[0][1]
+    cache = []
+    nb = (len(W) - 3) // 2
+    for i in range(nb):
+        (w1, b1), (w2, b2) = W[1 + 2 * i], W[2 + 2 * i]
+        a1 = x @ w1.T + b1
+        h1 = np.maximum(a1, 0.0)
+        a2 = h1 @ w2.T + b2
+        cache.append((x, a1, h1, a2))
+        x = x + np.maximum(a2, 0.0)
+    la = x @ W[-2][0].T + W[-2][1]
+    lf = x @ W[-1][0].T + W[-1][1]
+    return la[:, :-1], lf, la[:, -1:], (feats, cache, x)
+
+
+def _sigmoid(z):
+    out = np.empty_like(z)
+    pos = z >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-z[pos]))
+    ez = np.exp(z[~pos])
+    out[~pos] = ez / (1.0 + ez)
+    return out
+
+
+def bce_loss(logits, targets, row_mask=None):
+    """nn.py:178-196."""
+    per = np.maximum(logits, 0.0) - logits * targets + np.log1p(np.exp(-np.abs(logits)))
+    grad = _sigmoid(logits) - targets
+    if row_mask is not None:
+        per = per * row_mask[:, None]
+        grad = grad * row_mask[:, None]
+        count = int(row_mask.sum()) * logits.shape[1]
+    else:
+        count = logits.size
+    if count == 0:
+        return 0.0, np.zeros_like(logits)
+    return float(per.sum() / count), grad / count
+
+
+def backward(model: "OracleModel", cache, g_c, g_f, g_a):
+    """nn.py:138-167; gradients parallel to flat_params."""
+    feats, blocks, feat = cache
+    W = model.weights
+    gA = np.concatenate([g_c, g_a], axis=1)
+    out_tail_a = (gA.T @ feat, gA.sum(axis=0))
+    out_tail_b = (g_f.T @ feat, g_f.sum(axis=0))
+    g_x = gA @ W[-2][0] + g_f @ W[-1][0]
+    nb = len(blocks)
+    per_block = []
+    for i in reversed(range(nb)):
+        x, a1, h1, a2 = blocks[i]
+        (w1, _), (w2, _) = W[1 + 2 * i], W[2 + 2 * i]
+        g_a2 = np.where(a2 > 0, g_x, 0.0)
+        g_fc2 = (g_a2.T @ h1, g_a2.sum(axis=0))
+        g_h1 = g_a2 @ w2
+        g_a1 = np.where(a1 > 0, g_h1, 0.0)
+        g_fc1 = (g_a1.T @ x, g_a1.sum(axis=0))
+        per_block.append((g_fc1, g_fc2))
+        g_x = g_x + g_a1 @ w1
+    out = [g_x.T @ feats, g_x.sum(axis=0)]
+    for g_fc1, g_fc2 in reversed(per_block):
+        out.extend((g_fc1[0], g_fc1[1], g_fc2[0], g_fc2[1]))
+    out.extend((out_tail_a[0], out_tail_a[1], out_tail_b[0], out_tail_b[1]))
+    return out
+
+
+def loss_and_grads(model: "OracleModel", feats, coarse, fine, hit, n_coarse=64, n_fine=128):
+    """model.py:238-248 with bin indices (coarse / fine valid where hit) as targets."""
+    lc, lf, la, cache = forward_cached(model, feats)
+    n = feats.shape[0]
+    tc = np.zeros((n, n_coarse))
+    tf = np.zeros((n, n_fine))
+    rows = np.flatnonzero(hit)
+    tc[rows, coarse[rows]] = 1.0
+    tf[rows, fine[rows]] = 1.0
+    mask = hit.astype(np.float64)
+    loss_c, g_c = bce_loss(lc, tc, row_mask=mask)
+    loss_f, g_f = bce_loss(lf, tf, row_mask=mask)
+    loss_a, g_a = bce_loss(la, hit.astype(np.float64)[:, None])
+    total = loss_c + loss_f + 0.1 * loss_a
+    return total, (loss_c, loss_f, loss_a), backward(model, cache, g_c, g_f, 0.1 * g_a)
+
+
+def adam_step(params, grads, m, v, t, lr=5e-4, b1=0.9, b2=0.999, eps=1e-8):
+    """nn.py:218-232 (t = the step count after incrementing)."""
+    bc1 = 1.0 - b1 ** t
+    bc2 = 1.0 - b2 ** t
+    for p, g, mm, vv in zip(params, grads, m, v):
+        mm *= b1
+        mm += (1.0 - b1) * g
+        vv *= b2
+        vv += (1.0 - b2) * g * g
+        p -= lr * (mm / bc1) / (np.sqrt(vv / bc2) + eps)

@@ -107,6 +107,19 @@ PROTOTYPES = {
                                    C.POINTER(NedfField), C.c_int, C.POINTER(NedfLight),
                                    C.POINTER(NedfRenderConfig), C.POINTER(NedfFrameBuffers), P]),
     "nedf_composite": (C.c_int, [P, C.POINTER(NedfFrameBuffers), C.c_int, P]),
+    "nedf_to_u8": (C.c_int, [P, I64, P, P]),
+    "nedf_depth_to_f32": (C.c_int, [P, I64, P, P]),
+    "nedf_depth_to_gray": (C.c_int, [P, I64, P, P, P]),
+    "nedf_id_to_u16": (C.c_int, [P, I64, P, P]),
+    "nedf_trainer_last_error": (C.c_char_p, []),
+    "nedf_trainer_create": (C.c_int, [C.c_int, C.POINTER(NedfModelInfo), P, I64, C.c_int, C.POINTER(P)]),
+    "nedf_trainer_destroy": (None, [P]),
+    "nedf_trainer_set_lr": (C.c_int, [P, C.c_float]),
+    "nedf_trainer_batch": (C.c_int, [P, P, C.c_int, C.c_int, C.c_double, P, P, C.c_int, P, P]),
+    "nedf_trainer_set_batch": (C.c_int, [P, P, P, P, P, C.c_int, P]),
+    "nedf_trainer_loss_and_grads": (C.c_int, [P, P, P]),
+    "nedf_trainer_adam_step": (C.c_int, [P, P]),
+    "nedf_trainer_read": (C.c_int, [P, C.c_int, P, P]),
     "nedf_render_frame": (C.c_int, [P, C.POINTER(NedfCamera), C.POINTER(NedfObject), C.c_int,
                                     C.POINTER(NedfField), C.c_int, C.POINTER(NedfLight), C.c_int,
                                     C.POINTER(NedfRenderConfig), C.POINTER(NedfFrameBuffers), P]),

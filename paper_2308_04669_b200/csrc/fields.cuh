@@ -47,7 +47,7 @@ __device__ __forceinline__ double leaf_sdf(const NedfField& f, const double p[3]
 // Signed distance of a field tree (fields.py:57-186).  min distributes over
 // positive scales, so a DFS with a running min handles unions and nested
 // transforms without recursion.
-__device__ double field_sdf(const NedfField* fields, int root, const double p0[3]) {
+__device__ inline double field_sdf(const NedfField* fields, int root, const double p0[3]) {
   struct Frame { int node; double p[3]; double scale; };
   Frame st[12];
   int sp = 0;
@@ -78,7 +78,7 @@ __device__ double field_sdf(const NedfField* fields, int root, const double p0[3
 }
 
 // VoxelField.sample (fields.py:294-319)
-__device__ void voxel_sample(const NedfField& f, const double p[3], double rgb[3], double& sigma) {
+__device__ inline void voxel_sample(const NedfField& f, const double p[3], double rgb[3], double& sigma) {
   int res[3] = {f.res[0], f.res[1], f.res[2]};
   const double* bmin = f.p;
   const double* bmax = f.p + 3;
@@ -116,7 +116,7 @@ __device__ void voxel_sample(const NedfField& f, const double p[3], double rgb[3
 }
 
 // radiance(p, d) -> (rgb, sigma) of an appearance field (fields.py:249-259, 468-469, 502-504)
-__device__ void field_radiance(const NedfField* fields, int root, const double p[3], double rgb[3],
+__device__ inline void field_radiance(const NedfField* fields, int root, const double p[3], double rgb[3],
                                double& sigma) {
   const NedfField& f = fields[root];
   if (f.kind == NEDF_FIELD_VOXEL) {
@@ -135,7 +135,7 @@ __device__ void field_radiance(const NedfField* fields, int root, const double p
 
 // sphere_trace_batch for one ray + secant polish (fields.py:194-238).
 // Returns hit; t is the local depth.
-__device__ bool sphere_trace(const NedfField* fields, int root, const double o[3], const double d[3],
+__device__ inline bool sphere_trace(const NedfField* fields, int root, const double o[3], const double d[3],
                              double t_max, double& t_out) {
   double t = 0.0;
   if (field_sdf(fields, root, o) <= -kSurfaceEps) { t_out = 0.0; return true; }

@@ -108,6 +108,22 @@ class NedfModel:
     def nedm_bytes(self) -> bytes:
         return self._raw
 
+    def reload(self, raw: bytes) -> None:
+        """Replace the weights in place (after training) from a .nedm image of the
+        same dimensions; scene tables built afterwards see the new handle."""
+        h = C.c_void_p()
+        _lib.check(self._lib.nedf_model_load(self._ctx.handle, raw, len(raw), C.byref(h)))
+        info = _lib.NedfModelInfo()
+        _lib.check(self._lib.nedf_model_info(h, C.byref(info)))
+        if (info.d_in, info.d_feat, info.n_blocks) != (self.d_in, self.d_feat, self.n_blocks):
+            self._lib.nedf_model_free(h)
+            raise ValueError("reload: model dimensions differ")
+        old, self.handle = self.handle, h
+        self._raw = bytes(raw)
+        self.tensor_ok = bool(self._lib.nedf_model_tensor_ok(h))
+        if old:
+            self._lib.nedf_model_free(old)
+
     def __del__(self):
         try:
             if getattr(self, "handle", None):

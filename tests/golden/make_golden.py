@@ -251,7 +251,63 @@ def gen_extra():
          **out)
 
 
+def gen_imgio():
+    """Reference imgio.py conversions (to_u8, depth_to_gray, 16-bit id PNG values) on
+    planes with the edge cases: values around the u8 rounding boundaries, out of
+    range, misses (+inf), depth ties (round half to even), ids past 65534."""
+    from nedf import imgio
+    import io as _io
+    from PIL import Image
+    rng = np.random.default_rng(42)
+    rgb = rng.uniform(-0.2, 1.2, size=(16, 24, 3))
+    k = rng.integers(0, 256, size=(16, 24, 3))
+    rgb[::3] = (k[::3] + 0.5) / 255.0                        # exactly on rounding boundaries
+    rgb = rgb.astype(np.float32).astype(np.float64)          # the GPU image is float32
+    depth = rng.uniform(0.5, 9.0, size=(16, 24))
+    depth[rng.random((16, 24)) < 0.3] = np.inf
+    depth[0, :4] = [1.0, 2.0, 3.0, 1.0 + 8.0 * 0.5 / 255.0]
+    ids = rng.integers(-1, 70000, size=(16, 24)).astype(np.int32)
+    ids[0, :3] = [-1, 65534, 65535]
+    u16 = np.asarray(Image.open(_io.BytesIO(imgio.encode_id_png(ids))))
+    save("imgio.npz", rgb=rgb, u8=imgio.to_u8(rgb), depth=depth, gray=imgio.depth_to_gray(depth),
+         ids=ids, id_u16=u16.astype(np.uint16), depth_raw=np.frombuffer(_raw_depth(imgio, depth), dtype=np.uint8))
+
+
+def _raw_depth(imgio, depth):
+    import tempfile
+    with tempfile.NamedTemporaryFile(suffix=".ndpt") as f:
+        imgio.write_depth_raw(f.name, depth, 2.5)
+        return open(f.name, "rb").read()
+
+
+def gen_train():
+    """One reference training step (model.py:210-248, nn.py:218-232) on a desk-profile
+    sphere model (d_feat 64, 4 blocks) with f32-exact weights: the batch drawn by
+    RaySampler(seed 7, 256 rays), its targets, the three losses, all gradients and the
+    parameters after one Adam step."""
+    import tempfile
+    from nedf import model as M, nn
+    oracle = fields.AnalyticOracle(fields.Sphere(geometry.vec3(0, 0, 0), 1.0))
+    nm = M.new_model(oracle, np.random.default_rng(3), M.PROFILES["desk"])
+    with tempfile.NamedTemporaryFile(suffix=".nedm") as f:
+        M.save_nedf(nm, f.name)
+        raw = open(f.name, "rb").read()
+        nm = M.load_nedf(f.name)
+    sampler = M.RaySampler(box=nm.relaxed_box)
+    rng = np.random.default_rng(7)
+    origins, dirs = sampler.sample(np.random.default_rng(7), 256)      # the rays the batch draws first
+    batch = M.build_training_batch(oracle, sampler, nm.config, rng, batch_size=256)
+    total, parts, grads = M.loss_and_grads(nm.mlp, batch)
+    params = nm.mlp.parameters()
+    state = nn.AdamState.for_params(params, lr=5e-4)
+    nn.adam_step(state, params, grads)
+    flat = lambda xs: np.concatenate([np.asarray(x, dtype=np.float64).ravel() for x in xs])
+    save("train_step.npz", raw=np.frombuffer(raw, dtype=np.uint8), origins=origins, dirs=dirs,
+         feats=batch.encoded, coarse=batch.target_coarse.argmax(axis=1), fine=batch.target_fine.argmax(axis=1),
+         hit=batch.valid_mu, total=total, parts=np.array(parts), grads=flat(grads), params_after=flat(params))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["geometry", "models", "forward", "analytic", "frames", "extra"]
+    which = sys.argv[1:] or ["geometry", "models", "forward", "analytic", "frames", "extra", "imgio", "train"]
     for w in which:
         globals()[f"gen_{w}"]()

@@ -14,7 +14,7 @@ HEADER = ROOT / "include" / "nedf_b200.h"
 def declared_functions():
     text = HEADER.read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(nedf_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(nedf_[a-z0-9_]+)\s*\(", text)))
 
 
 @pytest.fixture(scope="module")
@@ -39,7 +39,7 @@ def test_every_header_symbol_is_exported(lib):
     """All of include/*.h (the public ABI and the diagnostics header)."""
     for h in sorted((ROOT / "include").glob("*.h")):
         text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
-        for name in sorted(set(re.findall(r"\b(nedf_[a-z_]+)\s*\(", text))):
+        for name in sorted(set(re.findall(r"\b(nedf_[a-z0-9_]+)\s*\(", text))):
             assert hasattr(lib, name), f"{h.name}: {name}"
 
 
