@@ -308,8 +308,17 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
             pend = (kc & 1) ? stage - 1 : -1;
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
-          if (L == kBodyLayers && tc::elect_one()) tc::mma_commit(&S.aq_free);   // last A_Q reader issued
-          __syncwarp();
+          if (L == kBodyLayers) {
+            // last A_Q reader issued.  The deferred release of layer 32's last stage pair goes out
+            // first: the encoders take point consumption from those pair barriers, and their
+            // parity is only meaningful once every earlier use has been committed.
+            if (tc::elect_one()) {
+              if (pend >= 0) tc::mma_commit_mc(&S.empty[pend], cmask);
+              tc::mma_commit(&S.aq_free);
+            }
+            __syncwarp();
+            pend = -1;
+          }
           trace_at(tr, 40 + L);
           ++layer_ctr;
         }

@@ -168,9 +168,29 @@ def sweep(flush, sizes=(1 << 16, 1 << 18, 1 << 20, 1 << 22, 1 << 24)):
     return out
 
 
+def training(flush):
+    """GPU distillation iterations/s (the reference's train loop, model.py:251-274) for the
+    desk and paper profiles on the unit sphere; batch 1024 / 4096 like TrainProfile."""
+    from paper_2308_04669_b200 import fields, train
+    out = []
+    for name, bs in (("desk", 1024), ("paper", 4096)):
+        oracle = fields.AnalyticOracle(fields.Sphere(geometry.vec3(0, 0, 0), 1.0))
+        m = model.new_model(oracle, np.random.default_rng(0), model.PROFILES[name])
+        train.train(m, oracle, np.random.default_rng(1), iterations=3, batch_size=bs)
+        torch.cuda.synchronize()
+        n = 20
+        t0 = time.perf_counter()
+        losses = train.train(m, oracle, np.random.default_rng(2), iterations=n, batch_size=bs)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / n
+        out.append({"workload": f"train {name} profile (batch {bs}), incl. host ray sampling", "ms_per_iteration": dt * 1e3,
+                    "iterations_per_s": 1.0 / dt, "rays_per_s": bs / dt, "final_loss": float(losses[-1])})
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="config1,config2,config3,config4,config5,sweep")
+    ap.add_argument("--only", default="config1,config2,config3,config4,config5,sweep,train")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     which = set(args.only.split(","))
@@ -202,6 +222,8 @@ def main():
         lines.append(config5(flush))
     if "sweep" in which:
         lines.extend(sweep(flush))
+    if "train" in which:
+        lines.extend(training(flush))
     if args.out:
         Path(args.out).write_text("".join(json.dumps(x) + "\n" for x in lines))
 

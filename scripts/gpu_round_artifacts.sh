@@ -3,13 +3,13 @@
 # list of the bench command and full captures of the network and guard kernels.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -1 gpurun_out/bench.json
-timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -1 gpurun_out/bench_ref.json
-timeout 900 python scripts/bench_configs.py --out gpurun_out/configs.jsonl > /dev/null 2> gpurun_out/configs.err; wc -l gpurun_out/configs.jsonl
+timeout 300 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -1 gpurun_out/bench.json
+timeout 300 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -1 gpurun_out/bench_ref.json
+timeout 400 python scripts/bench_configs.py --out gpurun_out/configs.jsonl > /dev/null 2> gpurun_out/configs.err; wc -l gpurun_out/configs.jsonl
 # launch list of the same command (cold-cache, serialised per-launch times)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launches.log 2>&1; echo launches rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:nedf_mlp_tc_kernel -s 2 -c 1 \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:nedf_mlp_tc_kernel -s 2 -c 1 \
   -o gpurun_out/tc_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_tc.log 2>&1; echo tc rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:mlp_fp32_cluster -s 2 -c 1 \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:mlp_fp32_cluster -s 2 -c 1 \
   -o gpurun_out/guard_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_guard.log 2>&1; echo guard rc=$?
