@@ -4,23 +4,31 @@
 //
 // Per CTA (one per SM), 16 warps in four warpgroups:
 //   warp 0        bulk-copy producer: streams the model's pre-swizzled fp16
-//                 operand image (296 x 16 KB stages per tile) into an 8-stage ring
+//                 operand image (296 x 16 KB stages per tile) into a 10-slot ring;
+//                 lane j owns slot j.  In clusters of csize CTAs (default 2) each
+//                 CTA fetches 1/csize of every stage and multicasts it to all
 //   warp 1        MMA issuer (warp-uniform loop, elect.sync issues) + TMEM owner
 //   warps 4-7     encoders: thread = ray; float64 ray setup, 16 sample points,
-//                 sinusoidal features -> fp16 A tiles (128B swizzle), 2-stage ring
+//                 sinusoidal features -> fp16, stored with tcgen05.st straight into
+//                 TMEM (4-point ring in the A_Q columns, free during the head)
 //   warps 8-15    epilogue: thread = (ray, 64-column half of each 128-column slice);
 //                 the fp32 residual stream x[256] lives in registers (128 per thread)
 //
 // TMEM (512 columns): [0,256) fp32 accumulator as two 128-column slices,
 // [256,384) A_P = fp16 x (input of fc1 and of the tails), [384,512) A_Q = fp16 h
-// (input of fc2).  The head uses the SS form (A = encoded rays in shared
-// memory, N = 256); all later layers use the TS form (A in TMEM, N = 128 per
-// slice), which measured 86% of the nominal tcgen05 rate at N = 128 versus
-// ~75% for the shared-memory-bound SS form.
+// (input of fc2; the encoded head points before layer 1).  Every layer uses the
+// TS form (A in TMEM): head M128 x N256 per point chunk, body and tail
+// M128 x N128 per slice (86% of the nominal tcgen05 rate measured at N = 128).
 //
 // Wavefront: layer L+1's MMAs for K chunks 0-1 depend only on the epilogue of
 // layer L's slice 0, so that epilogue overlaps the MMAs of slice 1, and the
 // epilogue of slice 1 overlaps the first half of layer L+1.
+//
+// Synchronisation cost: one tcgen05.commit releases a pair of weight slots, and
+// in the body it is issued after the next stage's wait together with that
+// stage's MMAs -- each commit -> wait round costs the tensor pipe a bubble
+// (scripts/mma_contention.py).  The head's encoders learn that a point slot is
+// free from the same pair barriers.
 //
 // Precision guard: fp16 operands / fp32 accumulation perturb the logits by up
 // to ~1.2e-3 of max|logit| (scripts/tc_calibrate.py); rays whose top-2 coarse
@@ -57,7 +65,7 @@ struct __align__(16) RowRed {
 
 struct TcShared {
   uint64_t full[kStages], empty[kStages];
-  uint64_t enc_full[kEncSlots], enc_empty[kEncSlots];
+  uint64_t enc_full[kEncSlots];   // point slot filled (4 encoder warps); emptied via the weight-pair barriers
   uint64_t aq_free;              // layer 32's MMAs (last readers of A_Q) completed: the next head may write A_Q
   uint64_t acc_full[2], epi_done[2];
   uint32_t tmem_base;
@@ -179,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
       S.tiles[g + 1] = cum;
     }
     for (int i = 0; i < kStages; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], csize); }
-    for (int i = 0; i < kEncSlots; ++i) { tc::mbar_init(&S.enc_full[i], 4); tc::mbar_init(&S.enc_empty[i], 1); }
+    for (int i = 0; i < kEncSlots; ++i) tc::mbar_init(&S.enc_full[i], 4);
     tc::mbar_init(&S.aq_free, 1);
     for (int i = 0; i < 2; ++i) { tc::mbar_init(&S.acc_full[i], 1); tc::mbar_init(&S.epi_done[i], 8); }
     tc::mbar_fence_init();
