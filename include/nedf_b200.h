@@ -187,6 +187,12 @@ int nedf_set_option(NedfContext* ctx, int key, int64_t value);
 int nedf_get_option(NedfContext* ctx, int key, int64_t* value);
 /* Device-side counters of the last step (evals, guarded, ...); synchronises `stream`. */
 int nedf_read_stats(NedfContext* ctx, NedfStepStats* out, void* stream);
+/* Non-blocking counterpart of nedf_read_stats: enqueue a copy of this step's device
+ * counters into mapped slot `slot` (0..63) and reset them; out receives the host-side
+ * counters (launches, h2d_bytes) now.  After the stream reaches this point (event or
+ * synchronize), nedf_stats_slot fills evals / guarded / covered / resampled from the slot. */
+int nedf_stats_snapshot(NedfContext* ctx, int slot, NedfStepStats* out, void* stream);
+int nedf_stats_slot(NedfContext* ctx, int slot, NedfStepStats* out);
 
 /* ---- weights (model.py:354-369, nn.py:235-281) ------------------------------ */
 /* Parse a .nedm image (header, f32 parameters, 7-f32 trailer) and upload the

@@ -107,6 +107,8 @@ PROTOTYPES = {
                                    C.POINTER(NedfField), C.c_int, C.POINTER(NedfLight),
                                    C.POINTER(NedfRenderConfig), C.POINTER(NedfFrameBuffers), P]),
     "nedf_composite": (C.c_int, [P, C.POINTER(NedfFrameBuffers), C.c_int, P]),
+    "nedf_stats_snapshot": (C.c_int, [P, C.c_int, C.POINTER(NedfStepStats), P]),
+    "nedf_stats_slot": (C.c_int, [P, C.c_int, C.POINTER(NedfStepStats)]),
     "nedf_to_u8": (C.c_int, [P, I64, P, P]),
     "nedf_depth_to_f32": (C.c_int, [P, I64, P, P]),
     "nedf_depth_to_gray": (C.c_int, [P, I64, P, P, P]),
@@ -189,6 +191,21 @@ class Context:
         return {"evals": s.evals, "guarded": s.guarded, "covered": s.covered, "resampled": s.resampled,
                 "launches": s.launches, "net_launches": s.net_launches, "net_ms": s.net_ms,
                 "guard_ms": s.guard_ms, "h2d_bytes": s.h2d_bytes}
+
+    def snapshot_stats(self, stream) -> tuple[int, dict]:
+        """Non-blocking: enqueue this step's counters into the next mapped slot; returns
+        (slot, host-side counters).  Resolve with `slot_stats(slot)` after the stream
+        passes this point.  64 slots rotate."""
+        slot = getattr(self, "_next_slot", 0)
+        self._next_slot = (slot + 1) % 64
+        s = NedfStepStats()
+        check(self._lib.nedf_stats_snapshot(self.handle, slot, C.byref(s), stream))
+        return slot, {"launches": s.launches, "h2d_bytes": s.h2d_bytes}
+
+    def slot_stats(self, slot: int) -> dict:
+        s = NedfStepStats()
+        check(self._lib.nedf_stats_slot(self.handle, slot, C.byref(s)))
+        return {"evals": s.evals, "guarded": s.guarded, "covered": s.covered, "resampled": s.resampled}
 
     def __del__(self):
         try:

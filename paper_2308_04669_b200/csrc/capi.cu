@@ -63,6 +63,8 @@ struct NedfModel {
   int device = 0;
 };
 
+constexpr int kStatSlots = 64;   // mapped snapshot slots (nedf_stats_snapshot)
+
 struct NedfContext {
   int device = 0;
   int n_sms = 148;
@@ -539,7 +541,9 @@ int nedf_context_create(int device, NedfContext** out) {
   NedfContext* c = new NedfContext();
   c->device = device;
   c->n_sms = prop.multiProcessorCount;
-  if (cudaHostAlloc(&c->stats_host, 8 * sizeof(unsigned long long), cudaHostAllocMapped) != cudaSuccess ||
+  // slot kStatSlots: nedf_read_stats; slots [0, kStatSlots): nedf_stats_snapshot
+  if (cudaHostAlloc(&c->stats_host, 8 * (kStatSlots + 1) * sizeof(unsigned long long), cudaHostAllocMapped) !=
+          cudaSuccess ||
       cudaHostGetDevicePointer(&c->stats_host_dev, c->stats_host, 0) != cudaSuccess) {
     if (c->stats_host) cudaFreeHost(c->stats_host);
     delete c;
@@ -598,14 +602,43 @@ int nedf_get_option(NedfContext* c, int key, int64_t* v) {
   return fail(NEDF_ERR_INVALID, "unknown option");
 }
 
+int nedf_stats_snapshot(NedfContext* c, int slot, NedfStepStats* out, void* stream) {
+  if (!c || !out) return fail(NEDF_ERR_INVALID, "NULL argument");
+  if (slot < 0 || slot >= kStatSlots) return fail(NEDF_ERR_INVALID, "stats slot out of range");
+  memset(out, 0, sizeof(*out));
+  if (c->stats.ptr) {
+    CUDA_TRY(launch_stats_export(c->stats.as<unsigned long long>(), c->stats_host_dev + 8 * slot,
+                                 (cudaStream_t)stream));
+  } else {
+    for (int i = 0; i < 8; ++i) c->stats_host[8 * slot + i] = 0;
+  }
+  out->launches = c->launches;
+  c->launches = 0;
+  out->h2d_bytes = c->h2d_bytes;
+  c->h2d_bytes = 0;
+  return NEDF_OK;
+}
+
+int nedf_stats_slot(NedfContext* c, int slot, NedfStepStats* out) {
+  if (!c || !out) return fail(NEDF_ERR_INVALID, "NULL argument");
+  if (slot < 0 || slot >= kStatSlots) return fail(NEDF_ERR_INVALID, "stats slot out of range");
+  const volatile unsigned long long* h = c->stats_host + 8 * slot;
+  out->covered = (int64_t)h[0];
+  out->resampled = (int64_t)h[1];
+  out->evals = (int64_t)h[2];
+  out->guarded = (int64_t)h[3];
+  return NEDF_OK;
+}
+
 int nedf_read_stats(NedfContext* c, NedfStepStats* out, void* stream) {
   if (!c || !out) return fail(NEDF_ERR_INVALID, "NULL argument");
   unsigned long long h[8] = {0};
   if (c->stats.ptr) {
     cudaStream_t st = (cudaStream_t)stream;
-    CUDA_TRY(launch_stats_export(c->stats.as<unsigned long long>(), c->stats_host_dev, st));
+    CUDA_TRY(launch_stats_export(c->stats.as<unsigned long long>(), c->stats_host_dev + 8 * kStatSlots, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    for (int i = 0; i < 8; ++i) h[i] = reinterpret_cast<volatile unsigned long long*>(c->stats_host)[i];
+    for (int i = 0; i < 8; ++i)
+      h[i] = reinterpret_cast<volatile unsigned long long*>(c->stats_host)[8 * kStatSlots + i];
   }
   out->covered = (int64_t)h[0];
   out->resampled = (int64_t)h[1];

@@ -417,10 +417,77 @@ def import_external_gbuffer(buffers: FrameBuffers, depth_plane, color_image, pse
     buffers.rgb[closer] = c[closer]
 
 
+class _LazyTiming(dict):
+    """RenderResult.timing without a host sync at the end of compose_frame: the
+    host-side entries (kernel_launches, h2d_bytes) are there at once; the first
+    access to anything else waits for the frame's last event and fills in the
+    step times and the device counters (from a mapped stats slot, valid for the
+    next 63 frames).  Behaves as a plain dict afterwards."""
+
+    _EAGER = ("kernel_launches", "h2d_bytes")
+
+    def __init__(self, eager: dict, resolve):
+        super().__init__(eager)
+        self._resolve = resolve
+
+    def _fill(self):
+        if self._resolve is not None:
+            r, self._resolve = self._resolve, None
+            dict.update(self, r())
+
+    def __getitem__(self, k):
+        if k not in self._EAGER:
+            self._fill()
+        return dict.__getitem__(self, k)
+
+    def get(self, k, default=None):
+        if k not in self._EAGER:
+            self._fill()
+        return dict.get(self, k, default)
+
+    def __contains__(self, k):
+        self._fill()
+        return dict.__contains__(self, k)
+
+    def __iter__(self):
+        self._fill()
+        return dict.__iter__(self)
+
+    def __len__(self):
+        self._fill()
+        return dict.__len__(self)
+
+    def keys(self):
+        self._fill()
+        return dict.keys(self)
+
+    def items(self):
+        self._fill()
+        return dict.items(self)
+
+    def values(self):
+        self._fill()
+        return dict.values(self)
+
+    def copy(self):
+        self._fill()
+        return dict(self)
+
+    def __eq__(self, other):
+        self._fill()
+        return dict.__eq__(self, other)
+
+    def __repr__(self):
+        self._fill()
+        return dict.__repr__(self)
+
+
 def compose_frame(scene, camera: Camera, lights, config: RenderConfig | None = None,
                   buffers: FrameBuffers | None = None, changed_ids=None, external=None) -> RenderResult:
     """Steps 1-3 and image = rgb * shadow (pipeline.py:430-468).  Timing is
-    measured with CUDA events per step (seconds, like the reference)."""
+    measured with CUDA events per step (seconds, like the reference).  The call
+    returns as soon as the frame is enqueued (no host synchronisation); reading
+    the buffers or most timing entries waits for it."""
     import torch
     config = config or RenderConfig()
     if buffers is None:
@@ -429,7 +496,7 @@ def compose_frame(scene, camera: Camera, lights, config: RenderConfig | None = N
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     ctx = _ctx(buffers)
     st = _lib.stream_handle()
-    ctx.read_stats(st)
+    ctx.snapshot_stats(st)                 # reset the per-frame counters (no sync)
     ev[0].record()
     if changed_ids is None:
         nedf_generation_step(scene, camera, buffers, _tables=tb)
@@ -445,18 +512,23 @@ def compose_frame(scene, camera: Camera, lights, config: RenderConfig | None = N
         for light in lights:
             shadow_step(scene, camera, buffers, light, config, _tables=tb)
     _lib.check(_lib.load_library().nedf_composite(ctx.handle, C.byref(buffers._c(tb.n_objs)), camera.width, st))
+    slot, host = ctx.snapshot_stats(st)
     ev[3].record()
-    stats = ctx.read_stats(st)   # synchronises the stream
-    timing = {
-        "step1_depth_id": ev[0].elapsed_time(ev[1]) / 1e3,
-        "step2_shading": ev[1].elapsed_time(ev[2]) / 1e3,
-        "resample_ratio": stats["resampled"] / float(camera.width * buffers.n_rows),
-        "step3_shadow": ev[2].elapsed_time(ev[3]) / 1e3,
-        "network_evals": stats["evals"],
-        "guarded_evals": stats["guarded"],
-        "kernel_launches": stats["launches"],
-        "h2d_bytes": stats["h2d_bytes"],
-    }
+    n_pix = float(camera.width * buffers.n_rows)
+
+    def resolve():
+        ev[3].synchronize()
+        dev = ctx.slot_stats(slot)
+        return {
+            "step1_depth_id": ev[0].elapsed_time(ev[1]) / 1e3,
+            "step2_shading": ev[1].elapsed_time(ev[2]) / 1e3,
+            "resample_ratio": dev["resampled"] / n_pix,
+            "step3_shadow": ev[2].elapsed_time(ev[3]) / 1e3,
+            "network_evals": dev["evals"],
+            "guarded_evals": dev["guarded"],
+        }
+
+    timing = _LazyTiming({"kernel_launches": host["launches"], "h2d_bytes": host["h2d_bytes"]}, resolve)
     return RenderResult(image=buffers.image, buffers=buffers, timing=timing)
 
 
