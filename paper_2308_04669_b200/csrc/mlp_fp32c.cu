@@ -1,12 +1,12 @@
-// fp32 network for small ray batches, split across a cluster of 8 CTAs.
+// fp32 network for small ray batches, split across a cluster of kC = 4 CTAs.
 //
 // Role: the near-tie guard's re-evaluation (a few hundred rays per frame).
 // Its cost is latency, not FLOPs: one ray still walks a 35-layer chain.  The
 // streaming kernel (mlp_fp32s.cu) runs that chain inside one SM, streaming the
-// whole 9.5 MB fp32 weight image through it.  Here the 8 CTAs of a cluster
-// share each ray tile: CTA r owns output columns [32 r, 32 r + 32) of every
-// layer, reads only its 1/8 of the weights (straight from L2, each thread a
-// contiguous 128-byte run per layer), and scatters its outputs into every
+// whole 9.5 MB fp32 weight image through it.  Here the 4 CTAs of a cluster
+// share each ray tile: CTA r owns output columns [64 r, 64 r + 64) of every
+// layer, reads only its 1/4 of the weights (straight from L2, each thread two
+// contiguous 128-byte chunks per layer), and scatters its outputs into every
 // peer's activation buffer with st.async through distributed shared memory.
 // Each store completes transaction bytes on the receiving CTA's mbarrier, so
 // a CTA starts layer L+1 as soon as all 16 KB of layer L have landed -- no
@@ -18,9 +18,13 @@
 // phase.  Same arithmetic as mlp_fp32s.cu: float64 features, float32 weights
 // and accumulation (a different summation order).
 //
-// Thread layout (256 threads): column quad cg = lane & 7 (columns 4 cg .. 4 cg + 3
-// of the CTA's 32), K part kp = 4 warp + (lane >> 3) of 32 (8 K rows per layer,
-// 32 for the head), so every x value loaded from shared memory feeds 4 FMAs.
+// Thread layout (256 threads): column quad cg = lane & 15 (columns 4 cg .. 4 cg + 3
+// of the CTA's 64), K part kp = 2 warp + (lane >> 4) of 16 (16 K rows per layer,
+// 64 for the head), so every x value loaded from shared memory feeds 4 FMAs.
+// Cluster size: 4 CTAs x ~130 KB of shared memory lets ~35 clusters (140 SMs)
+// co-reside, so a frame's guard batch is one round of 16-ray tiles; with 8 CTAs
+// per cluster (18 clusters) it took two rounds.  kC = 8 still compiles (the
+// constants below derive from it).
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -34,23 +38,31 @@
 namespace nedf {
 namespace {
 
-constexpr int kC = 8;                 // CTAs per cluster
-constexpr int kThreads = 256;         // 32 K parts x 8 column quads
-constexpr int kKP = 32;               // K parts
+#ifndef NEDF_GUARD_CLUSTER
+#define NEDF_GUARD_CLUSTER 4
+#endif
+constexpr int kC = NEDF_GUARD_CLUSTER;   // CTAs per cluster (4: ~35 co-resident, one round per frame step)
+static_assert(kC == 4 || kC == 8, "guard cluster size");
+constexpr int kCols = 256 / kC;       // output columns per CTA
+constexpr int kQuads = kCols / 4;     // column quads per CTA (one per lane group)
+constexpr int kLanesK = 32 / kQuads;  // K parts per warp
+constexpr int kThreads = 256;         // kKP K parts x kQuads column quads
+constexpr int kKP = 8 * kLanesK;      // K parts (8 warps)
 constexpr int kR = 16;                // rays per cluster tile
 constexpr int kHeadK = 1024;          // 16 points x (63 features + 1 zero)
 constexpr int kChunk = 32;            // weights per thread per chunk: 8 K rows x 4 columns
-constexpr int kHeadChunks = kHeadK / kKP / 8;   // 4
+constexpr int kHeadChunks = kHeadK / kKP / 8;   // 8-row chunks per thread: head
+constexpr int kBodyChunks = 256 / kKP / 8;      // body / tail
 constexpr int kLayers = 34;           // head, 32 block layers, fused tail
-constexpr int kChunks = kHeadChunks + kLayers - 1;                   // 37
+constexpr int kChunks = kHeadChunks + (kLayers - 1) * kBodyChunks;
 constexpr size_t kHeadFloats = (size_t)kC * kThreads * kHeadChunks * kChunk;   // 262144
-constexpr size_t kLayerFloats = (size_t)kC * kThreads * kChunk;                // 65536
+constexpr size_t kLayerFloats = (size_t)kC * kThreads * kBodyChunks * kChunk;  // 65536
 
 struct ClSmem {
   float f[kR][kHeadK];
   float x[kR][256];
   float h[kR][256];
-  float part[kKP / 4][kR][32];   // per warp (4 K parts, pre-reduced by shuffle)
+  float part[8][kR][kCols];      // per warp (its K parts pre-reduced by shuffle)
   double ray[kR][8];
   uint32_t pix[kR], obj[kR];
   int valid[kR];
@@ -64,6 +76,11 @@ constexpr uint32_t kLayerBytes = kR * 256 * 4;
 __device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uint32_t mbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr),
                "f"(a), "f"(b), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t addr, float a, float b, float c, float d, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+               "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar)
                : "memory");
 }
 __device__ __forceinline__ void st_async_f32(uint32_t addr, float v, uint32_t mbar) {
@@ -86,7 +103,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
   __shared__ int s_tiles[65];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int cg = lane & 7, kp = 4 * warp + (lane >> 3);
+  const int cg = lane % kQuads, kp = kLanesK * warp + lane / kQuads;
   const uint32_t rank = tc::cluster_rank();
   const int cid = blockIdx.x / kC, n_cl = gridDim.x / kC;
   const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
@@ -144,11 +161,13 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
     }
     __syncthreads();
     if (tr) g_cl_trace[64 * ti + 1] = clock64();
-    // ---- head features: this CTA computes sample points 2 rank, 2 rank + 1 and broadcasts them
+    // ---- head features: this CTA computes sample points kPtsPerCta rank .. kPtsPerCta (rank + 1) - 1 and broadcasts them
     // (float64, geometry.py:312-342); one (ray, point, coordinate, level) per thread
-    for (int e = tid; e < kR * 2 * 33; e += kThreads) {
-      const int r = e / 66, rem = e % 66, p2 = rem / 33, a = (rem / 11) % 3, lev = rem % 11;
-      const int pt = 2 * (int)rank + p2;
+    constexpr int kPtsPerCta = kPoints / kC;
+    for (int e = tid; e < kR * kPtsPerCta * 33; e += kThreads) {
+      const int r = e / (kPtsPerCta * 33), rem = e % (kPtsPerCta * 33), p2 = rem / 33, a = (rem / 11) % 3,
+                lev = rem % 11;
+      const int pt = kPtsPerCta * (int)rank + p2;
       float v0 = 0.f, v1 = 0.f;       // lev < 10: sin, cos; lev 10: raw p, pad
       if (S.valid[r]) {
         if (feats_in) {
@@ -195,7 +214,8 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
     auto chunk_ptr = [&](int q) -> const float4* {
       const size_t t = (size_t)rank * kThreads + tid;
       const float* p = q < kHeadChunks ? wl + (t * kHeadChunks + q) * kChunk
-                                       : wl + kHeadFloats + (size_t)(q - kHeadChunks) * kLayerFloats + t * kChunk;
+                                       : wl + kHeadFloats + (size_t)((q - kHeadChunks) / kBodyChunks) * kLayerFloats +
+                                             (t * kBodyChunks + (q - kHeadChunks) % kBodyChunks) * kChunk;
       return reinterpret_cast<const float4*>(p);
     };
     float4 wcur[8], wnxt[8];
@@ -204,15 +224,23 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) wcur[i] = __ldg(p + i);
     }
-    const int rr = tid >> 4, cc2 = 2 * (tid & 15), col2 = 32 * (int)rank + cc2;   // reduce role
-    float2 bnext = __ldg(reinterpret_cast<const float2*>(bias_p + col2));
+    constexpr int kOut = kCols / 16;                 // outputs per thread in the reduce phase (2 or 4)
+    const int rr = tid >> 4, cc2 = kOut * (tid & 15), col2 = kCols * (int)rank + cc2;   // reduce role
+    float bnext[kOut];
+#pragma unroll
+    for (int u = 0; u < kOut; ++u) bnext[u] = __ldg(bias_p + col2 + u);
     int q = 0;
     for (int L = 0; L < kLayers; ++L) {
-      const int nch = L == 0 ? kHeadChunks : 1;
+      const int nch = L == 0 ? kHeadChunks : kBodyChunks;
       const float* in = L == 0 ? &S.f[0][0] : ((L & 1) ? &S.x[0][0] : &S.h[0][0]);
       const int ld_in = L == 0 ? kHeadK : 256;
-      const float2 b = bnext;
-      if (L + 1 < kLayers) bnext = __ldg(reinterpret_cast<const float2*>(bias_p + (L + 1) * 256 + col2));
+      float b[kOut];
+#pragma unroll
+      for (int u = 0; u < kOut; ++u) b[u] = bnext[u];
+      if (L + 1 < kLayers) {
+#pragma unroll
+        for (int u = 0; u < kOut; ++u) bnext[u] = __ldg(bias_p + (L + 1) * 256 + col2 + u);
+      }
       float a[kR][4];
 #pragma unroll
       for (int r = 0; r < kR; ++r) a[r][0] = a[r][1] = a[r][2] = a[r][3] = 0.f;
@@ -249,42 +277,49 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       }
       if (tr && L == 5) g_cl_trace[64 * ti + 41] = clock64();
       if (g_cl_trace_on && cid == 0 && rank == 0 && lane == 0 && ti == 0 && L == 5) g_cl_trace[200 + warp] = clock64();
-      // pre-reduce the warp's four K parts (lanes l, l + 8, l + 16, l + 24), then across the 8 warps
+      // pre-reduce the warp's K parts (lanes l, l + kQuads, ...), then across the 8 warps
 #pragma unroll
       for (int r = 0; r < kR; ++r)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          a[r][u] += __shfl_xor_sync(0xffffffffu, a[r][u], 8);
-          a[r][u] += __shfl_xor_sync(0xffffffffu, a[r][u], 16);
-        }
-      if (lane < 8) {
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int off = kQuads; off < 32; off <<= 1) a[r][u] += __shfl_xor_sync(0xffffffffu, a[r][u], off);
+      if (lane < kQuads) {
 #pragma unroll
         for (int r = 0; r < kR; ++r)
           *reinterpret_cast<float4*>(&S.part[warp][r][4 * cg]) = make_float4(a[r][0], a[r][1], a[r][2], a[r][3]);
       }
       __syncthreads();
       if (tr && L == 5) g_cl_trace[64 * ti + 42] = clock64();
-      {   // two adjacent outputs per thread: 16 rays x 32 columns
-        float s0 = 0.f, s1 = 0.f;
+      {   // kOut adjacent outputs per thread: 16 rays x kCols columns
+        float sv[kOut];
 #pragma unroll
-        for (int w = 0; w < kKP / 4; ++w) {
-          const float2 pv = *reinterpret_cast<const float2*>(&S.part[w][rr][cc2]);
-          s0 += pv.x;
-          s1 += pv.y;
-        }
-        float v0, v1;
+        for (int u = 0; u < kOut; ++u) sv[u] = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+#pragma unroll
+          for (int u = 0; u < kOut; ++u) sv[u] += S.part[w][rr][cc2 + u];
+        float v[kOut];
         float* dst;
-        if (L == 0) { v0 = s0 + b.x; v1 = s1 + b.y; dst = &S.x[rr][col2]; }                     // head
-        else if (L == kLayers - 1) { v0 = s0 + b.x; v1 = s1 + b.y; dst = &S.h[rr][col2]; }       // tail logits
-        else if (L & 1) { v0 = fmaxf(s0 + b.x, 0.f); v1 = fmaxf(s1 + b.y, 0.f); dst = &S.h[rr][col2]; }   // fc1
-        else {                                                                                 // fc2 + residual
-          v0 = S.x[rr][col2] + fmaxf(s0 + b.x, 0.f);
-          v1 = S.x[rr][col2 + 1] + fmaxf(s1 + b.y, 0.f);
+        if (L == 0 || L == kLayers - 1) {                         // head (no activation) / tail logits
+#pragma unroll
+          for (int u = 0; u < kOut; ++u) v[u] = sv[u] + b[u];
+          dst = L == 0 ? &S.x[rr][col2] : &S.h[rr][col2];
+        } else if (L & 1) {                                       // fc1
+#pragma unroll
+          for (int u = 0; u < kOut; ++u) v[u] = fmaxf(sv[u] + b[u], 0.f);
+          dst = &S.h[rr][col2];
+        } else {                                                  // fc2 + residual
+#pragma unroll
+          for (int u = 0; u < kOut; ++u) v[u] = S.x[rr][col2 + u] + fmaxf(sv[u] + b[u], 0.f);
           dst = &S.x[rr][col2];
         }
         const int lb = layer_count & 1;
 #pragma unroll
-        for (int qq = 0; qq < kC; ++qq) st_async_v2(remote(qq, dst), v0, v1, remote(qq, &S.layer_bar[lb]));
+        for (int qq = 0; qq < kC; ++qq) {
+          if constexpr (kOut == 4) st_async_v4(remote(qq, dst), v[0], v[1], v[2], v[3], remote(qq, &S.layer_bar[lb]));
+          else st_async_v2(remote(qq, dst), v[0], v[1], remote(qq, &S.layer_bar[lb]));
+        }
       }
       if (tr && L == 5) g_cl_trace[64 * ti + 43] = clock64();
       if (tid == 0) tc::mbar_expect_tx(&S.layer_bar[layer_count & 1], kLayerBytes);
@@ -382,12 +417,12 @@ cudaError_t fp32_pack_cluster(const float* P, int d_in, int F, int n_blocks, int
     return 0.f;
   };
   for (int L = 0; L < kLayers; ++L) {
-    const int nch = L == 0 ? kHeadChunks : 1;
+    const int nch = L == 0 ? kHeadChunks : kBodyChunks;
     float* base = img.data() + (L == 0 ? 0 : kHeadFloats + (size_t)(L - 1) * kLayerFloats);
     for (int r = 0; r < kC; ++r)
       for (int t = 0; t < kThreads; ++t) {
-        const int cg = t & 7, kp = 4 * (t >> 5) + ((t >> 3) & 3);
-        const int c0 = 32 * r + 4 * cg;
+        const int lane = t & 31, cg = lane % kQuads, kp = kLanesK * (t >> 5) + lane / kQuads;
+        const int c0 = kCols * r + 4 * cg;
         for (int j = 0; j < nch; ++j) {
           float* dst = base + (((size_t)r * kThreads + t) * nch + j) * kChunk;
           for (int i = 0; i < 8; ++i) {
