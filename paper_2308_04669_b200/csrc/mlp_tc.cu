@@ -88,14 +88,12 @@ __device__ __forceinline__ void tile_lookup(const int* tiles, int ng, int t, con
 }
 
 // argmax bookkeeping: first maximum wins, `second` is the runner-up value
+// (branch-free: v > best moves best to second; v <= best makes second max(second, v); NaN changes nothing)
 __device__ __forceinline__ void top2_push(float v, int col, float& best, float& second, int& idx) {
-  if (v > best) {
-    second = best;
-    best = v;
-    idx = col;
-  } else if (v > second) {
-    second = v;
-  }
+  const bool up = v > best;
+  second = fmaxf(second, fminf(v, best));
+  idx = up ? col : idx;
+  best = up ? v : best;
 }
 
 // Features of one sample coordinate for the fp16 tensor-core path:
@@ -536,22 +534,27 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
             alpha = 0.f;
       int fidx = 0, cidx = 0;
       bool finite = true;
+      // both slices are loaded and released before any decoding: the next tile's head MMAs wait
+      // only for the tail MMAs, not for this epilogue's argmax work
+      uint32_t vt[2][2][32];                 // [slice][32-column part][column]
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         tc::mbar_wait(&S.acc_full[s], layer_ctr & 1);
         tc::tc_fence_after();
         trace_at(tr, 100 + 33 * 8 + s);
-        uint32_t vv2[2][32];               // both 32-column parts loaded, then the slice is released
-        tc::tmem_ld32(lane_addr + kAccCol + 128 * s + 64 * hc, vv2[0]);
-        tc::tmem_ld32(lane_addr + kAccCol + 128 * s + 64 * hc + 32, vv2[1]);
+        tc::tmem_ld32(lane_addr + kAccCol + 128 * s + 64 * hc, vt[s][0]);
+        tc::tmem_ld32(lane_addr + kAccCol + 128 * s + 64 * hc + 32, vt[s][1]);
         tc::tmem_ld_wait();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&S.epi_done[s]);
+      }
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
 #pragma unroll
         for (int j2 = 0; j2 < 2; ++j2) {
           const int col = 128 * s + 64 * hc + 32 * j2;
-          const uint32_t* v = vv2[j2];
+          const uint32_t* v = vt[s][j2];
           if (s == 1 && hc == 1) {         // alpha logit at tail column 192, then padding
             if (j2 == 0) {
               alpha = __uint_as_float(v[0]) + bt[192];
