@@ -5,26 +5,30 @@
 // streaming kernel (mlp_fp32s.cu) runs that chain inside one SM, streaming the
 // whole 9.5 MB fp32 weight image through it.  Here the 4 CTAs of a cluster
 // share each ray tile: CTA r owns output columns [64 r, 64 r + 64) of every
-// layer, reads only its 1/4 of the weights (straight from L2, each thread two
-// contiguous 128-byte chunks per layer), and scatters its outputs into every
-// peer's activation buffer with st.async through distributed shared memory.
-// Each store completes transaction bytes on the receiving CTA's mbarrier, so
-// a CTA starts layer L+1 as soon as all 16 KB of layer L have landed -- no
-// cluster-wide barrier (whose release semantics would also drain the weight
-// prefetch) per layer.  Buffer reuse is safe without one: a CTA can only
-// produce layer L+1 after receiving every peer's layer-L outputs, i.e. after
-// every peer finished reading the buffer layer L+1 overwrites.  Two layer
-// barriers alternate so a peer one layer ahead never completes the current
-// phase.  Same arithmetic as mlp_fp32s.cu: float64 features, float32 weights
-// and accumulation (a different summation order).
+// layer, so it needs only its 1/4 of the weights, and scatters its outputs into
+// every peer's activation buffer with st.async through distributed shared
+// memory.  Each store completes transaction bytes on the receiving CTA's
+// mbarrier, so a CTA starts layer L+1 as soon as all 16 KB of layer L have
+// landed -- no cluster-wide barrier per layer.  Buffer reuse is safe without
+// one: a CTA can only produce layer L+1 after receiving every peer's layer-L
+// outputs, i.e. after every peer finished reading the buffer layer L+1
+// overwrites.  Two layer barriers alternate so a peer one layer ahead never
+// completes the current phase.  Same arithmetic as mlp_fp32s.cu: float64
+// features, float32 weights and accumulation (a different summation order).
 //
-// Thread layout (256 threads): column quad cg = lane & 15 (columns 4 cg .. 4 cg + 3
-// of the CTA's 64), K part kp = 2 warp + (lane >> 4) of 16 (16 K rows per layer,
-// 64 for the head), so every x value loaded from shared memory feeds 4 FMAs.
-// Cluster size: 4 CTAs x ~130 KB of shared memory lets ~35 clusters (140 SMs)
-// co-reside, so a frame's guard batch is one round of 16-ray tiles; with 8 CTAs
-// per cluster (18 clusters) it took two rounds.  kC = 8 still compiles (the
-// constants below derive from it).
+// Weights: a producer warp (warp 8) streams the CTA's slice of the image as
+// 32 KB stages (one 8 K-row x 4-column chunk per compute thread; the head is 8
+// stages, every later layer 2) through a 3-slot shared-memory ring with bulk
+// copies, so the compute warps never wait on L2 latency; a compute warp copies
+// its chunk into registers and releases the slot before its FMAs.  The FMAs are
+// FFMA2 (fma.rn.f32x2: one x value times a pair of columns), the same fp32
+// operations in the same order as scalar FMAs, at half the issue slots.
+//
+// Thread layout (256 compute threads): column quad cg = lane & 15 (columns 4 cg
+// .. 4 cg + 3 of the CTA's 64), K part kp = 2 warp + (lane >> 4) of 16 (16 K rows
+// per layer, 64 for the head), so every x value loaded from shared memory feeds
+// 4 FMAs.  Cluster size: 4 CTAs lets ~35 clusters (140 SMs) co-reside, so a
+// frame's guard batch is one round of 16-ray tiles.
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -38,27 +42,26 @@
 namespace nedf {
 namespace {
 
-#ifndef NEDF_GUARD_CLUSTER
-#define NEDF_GUARD_CLUSTER 4
-#endif
-constexpr int kC = NEDF_GUARD_CLUSTER;   // CTAs per cluster (4: ~35 co-resident, one round per frame step)
-static_assert(kC == 4 || kC == 8, "guard cluster size");
-constexpr int kCols = 256 / kC;       // output columns per CTA
+constexpr int kC = 4;                 // CTAs per cluster
+constexpr int kCols = 256 / kC;       // output columns per CTA (64)
 constexpr int kQuads = kCols / 4;     // column quads per CTA (one per lane group)
 constexpr int kLanesK = 32 / kQuads;  // K parts per warp
-constexpr int kThreads = 256;         // kKP K parts x kQuads column quads
+constexpr int kThreads = 256;         // compute threads: kKP K parts x kQuads column quads
+constexpr int kBlock = kThreads + 32; // + the weight producer warp
 constexpr int kKP = 8 * kLanesK;      // K parts (8 warps)
 constexpr int kR = 16;                // rays per cluster tile
 constexpr int kHeadK = 1024;          // 16 points x (63 features + 1 zero)
 constexpr int kChunk = 32;            // weights per thread per chunk: 8 K rows x 4 columns
-constexpr int kHeadChunks = kHeadK / kKP / 8;   // 8-row chunks per thread: head
-constexpr int kBodyChunks = 256 / kKP / 8;      // body / tail
+constexpr int kHeadChunks = kHeadK / kKP / 8;   // 8-row chunks per thread: head (8)
+constexpr int kBodyChunks = 256 / kKP / 8;      // body / tail (2)
 constexpr int kLayers = 34;           // head, 32 block layers, fused tail
-constexpr int kChunks = kHeadChunks + (kLayers - 1) * kBodyChunks;
-constexpr size_t kHeadFloats = (size_t)kC * kThreads * kHeadChunks * kChunk;   // 262144
-constexpr size_t kLayerFloats = (size_t)kC * kThreads * kBodyChunks * kChunk;  // 65536
+constexpr int kStagesPerTile = kHeadChunks + (kLayers - 1) * kBodyChunks;       // 74
+constexpr uint32_t kStageBytes = kThreads * kChunk * 4;                         // 32 KB
+constexpr int kRing = 3;
+constexpr size_t kImageFloats = (size_t)kStagesPerTile * kC * kThreads * kChunk;
 
 struct ClSmem {
+  float4 ring[kRing][kStageBytes / 16];   // stage slot: float4 i of thread t at [8 i... see fp32_pack_cluster]
   float f[kR][kHeadK];
   float x[kR][256];
   float h[kR][256];
@@ -66,8 +69,9 @@ struct ClSmem {
   double ray[kR][8];
   uint32_t pix[kR], obj[kR];
   int valid[kR];
-  uint64_t feat_bar;             // features of the tile: 64 KB from the 8 CTAs
-  uint64_t layer_bar[2];         // layer L outputs (16 KB from the 8 CTAs) on layer_bar[L & 1]
+  uint64_t full[kRing], empty[kRing];
+  uint64_t feat_bar;             // features of the tile: 64 KB from the 4 CTAs
+  uint64_t layer_bar[2];         // layer L outputs (16 KB from the 4 CTAs) on layer_bar[L & 1]
 };
 constexpr uint32_t kFeatBytes = kR * kHeadK * 4;
 constexpr uint32_t kLayerBytes = kR * 256 * 4;
@@ -88,6 +92,24 @@ __device__ __forceinline__ void st_async_f32(uint32_t addr, float v, uint32_t mb
                "r"(mbar)
                : "memory");
 }
+// acc (two fp32 lanes) += x * (w0, w1), each lane one fma.rn.f32
+__device__ __forceinline__ uint64_t ffma2(float x, uint64_t w, uint64_t acc) {
+  uint64_t d;
+  asm("{\n\t.reg .b64 xx;\n\tmov.b64 xx, {%1, %1};\n\tfma.rn.f32x2 %0, xx, %2, %3;\n\t}"
+      : "=l"(d)
+      : "f"(x), "l"(w), "l"(acc));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_as_u64(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ float2 u64_as_f2(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
 
 }  // namespace
 
@@ -96,24 +118,17 @@ __device__ __forceinline__ void st_async_f32(uint32_t addr, float v, uint32_t mb
 __device__ unsigned long long g_cl_trace[256];
 __device__ int g_cl_trace_on;
 
-__global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kBlock, 1)
 mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   ClSmem& S = *reinterpret_cast<ClSmem*>(smem_raw);
   __shared__ int s_tiles[65];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int cg = lane % kQuads, kp = kLanesK * warp + lane / kQuads;
   const uint32_t rank = tc::cluster_rank();
   const int cid = blockIdx.x / kC, n_cl = gridDim.x / kC;
   const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
   const bool feats_in = out.feats != nullptr;
-  // shared::cluster address of S in every CTA of the cluster
-  uint32_t peer[kC];
-#pragma unroll
-  for (int q = 0; q < kC; ++q) peer[q] = tc::peer_addr(&S, q);
-  const uint32_t self = tc::smem_u32(&S);
-  auto remote = [&](int q, const void* p) { return peer[q] + (uint32_t)(tc::smem_u32(p) - self); };
 
   if (tid == 0) {
     int cum = 0;
@@ -122,6 +137,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       cum += (ls.count[g] + kR - 1) / kR;
       s_tiles[g + 1] = cum;
     }
+    for (int i = 0; i < kRing; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], 8); }
     tc::mbar_init(&S.feat_bar, 1);
     tc::mbar_init(&S.layer_bar[0], 1);
     tc::mbar_init(&S.layer_bar[1], 1);
@@ -129,7 +145,38 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
   }
   tc::cluster_sync();           // peers' barriers initialised before anyone stores into them
   const int total = s_tiles[ng];
-  uint32_t feat_phase = 0, layer_count = 0;
+
+  if (warp == 8) {
+    // ---------------------------------------------------------------- weight producer
+    // stage q of a tile = this CTA's 32 KB slice of (head chunk q | layer 1 + (q - 8) / 2, chunk (q - 8) % 2)
+    if (lane == 0) {
+      uint32_t gq = 0;
+      for (int t = cid; t < total; t += n_cl) {
+        int g = 0;
+        while (g < ng - 1 && t >= s_tiles[g + 1]) ++g;
+        const unsigned char* img = reinterpret_cast<const unsigned char*>(gt.models[g].wcluster);
+        for (int q = 0; q < kStagesPerTile; ++q, ++gq) {
+          const int slot = gq % kRing;
+          tc::mbar_wait(&S.empty[slot], ((gq / kRing) & 1) ^ 1);
+          tc::mbar_expect_tx(&S.full[slot], kStageBytes);
+          tc::bulk_g2s(&S.ring[slot][0], img + ((size_t)q * kC + rank) * kStageBytes, kStageBytes, &S.full[slot]);
+        }
+      }
+    }
+    __syncwarp();
+    tc::cluster_sync();
+    return;
+  }
+
+  // ------------------------------------------------------------------ compute warps
+  const int cg = lane % kQuads, kp = kLanesK * warp + lane / kQuads;
+  // shared::cluster address of S in every CTA of the cluster
+  uint32_t peer[kC];
+#pragma unroll
+  for (int q = 0; q < kC; ++q) peer[q] = tc::peer_addr(&S, q);
+  const uint32_t self = tc::smem_u32(&S);
+  auto remote = [&](int q, const void* p) { return peer[q] + (uint32_t)(tc::smem_u32(p) - self); };
+  uint32_t feat_phase = 0, layer_count = 0, gq = 0;
   int ti = 0;
   for (int t = cid; t < total; t += n_cl, ++ti) {
     const bool tr = g_cl_trace_on && cid == 0 && rank == 0 && tid == 0 && ti < 4;
@@ -159,7 +206,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
         S.ray[r][7] = t1;
       }
     }
-    __syncthreads();
+    tc::named_bar(1, kThreads);
     if (tr) g_cl_trace[64 * ti + 1] = clock64();
     // ---- head features: this CTA computes sample points kPtsPerCta rank .. kPtsPerCta (rank + 1) - 1 and broadcasts them
     // (float64, geometry.py:312-342); one (ray, point, coordinate, level) per thread
@@ -206,30 +253,12 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
     feat_phase ^= 1;
     if (tr) g_cl_trace[64 * ti + 2] = clock64();
     // ---- 34 layers: head (K = 1024), 16 x (fc1, fc2), fused tail (nn.py:115-135)
-    // The thread's weights stream as 37 chunks of 16 floats (head 4, then one per layer); the
-    // next chunk is loaded into registers while the current one is multiplied, so L2 latency
-    // overlaps the FMAs and the exchange.
-    const float* wl = m.wcluster;
     const float* bias_p = m.bias_pack;
-    auto chunk_ptr = [&](int q) -> const float4* {
-      const size_t t = (size_t)rank * kThreads + tid;
-      const float* p = q < kHeadChunks ? wl + (t * kHeadChunks + q) * kChunk
-                                       : wl + kHeadFloats + (size_t)((q - kHeadChunks) / kBodyChunks) * kLayerFloats +
-                                             (t * kBodyChunks + (q - kHeadChunks) % kBodyChunks) * kChunk;
-      return reinterpret_cast<const float4*>(p);
-    };
-    float4 wcur[8], wnxt[8];
-    {
-      const float4* p = chunk_ptr(0);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) wcur[i] = __ldg(p + i);
-    }
-    constexpr int kOut = kCols / 16;                 // outputs per thread in the reduce phase (2 or 4)
+    constexpr int kOut = kCols / 16;                 // outputs per thread in the reduce phase (4)
     const int rr = tid >> 4, cc2 = kOut * (tid & 15), col2 = kCols * (int)rank + cc2;   // reduce role
     float bnext[kOut];
 #pragma unroll
     for (int u = 0; u < kOut; ++u) bnext[u] = __ldg(bias_p + col2 + u);
-    int q = 0;
     for (int L = 0; L < kLayers; ++L) {
       const int nch = L == 0 ? kHeadChunks : kBodyChunks;
       const float* in = L == 0 ? &S.f[0][0] : ((L & 1) ? &S.x[0][0] : &S.h[0][0]);
@@ -241,17 +270,24 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
 #pragma unroll
         for (int u = 0; u < kOut; ++u) bnext[u] = __ldg(bias_p + (L + 1) * 256 + col2 + u);
       }
-      float a[kR][4];
+      uint64_t acc[kR][2];                           // columns (4 cg, 4 cg + 1), (4 cg + 2, 4 cg + 3)
 #pragma unroll
-      for (int r = 0; r < kR; ++r) a[r][0] = a[r][1] = a[r][2] = a[r][3] = 0.f;
-      // chunks alternate between two register buffers (no copy, which would wait on the prefetch)
-      auto run_chunk = [&](int j, float4 (&wc)[8], float4 (&wn)[8]) {
-        if (q + 1 < kChunks) {
-          const float4* p = chunk_ptr(q + 1);
+      for (int r = 0; r < kR; ++r) acc[r][0] = acc[r][1] = 0ull;
+      for (int j = 0; j < nch; ++j) {
+        // this chunk's weights: float4 i = W[c0 .. c0 + 3][k0 + i], copied out of the ring slot, which is
+        // then released to the producer before the FMAs
+        const int slot = gq % kRing;
+        tc::mbar_wait(&S.full[slot], (gq / kRing) & 1);
+        ++gq;
+        uint64_t w[8][2];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) wn[i] = __ldg(p + i);
+        for (int i = 0; i < 8; ++i) {
+          const float4 v = S.ring[slot][kThreads * i + tid];
+          w[i][0] = f2_as_u64(v.x, v.y);
+          w[i][1] = f2_as_u64(v.z, v.w);
         }
-        // this chunk's 8 K rows; float4 i = W[c0 .. c0 + 3][k0 + i]
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.empty[slot]);
         const float* inp = in + kp * (8 * nch) + 8 * j;
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
@@ -261,23 +297,21 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
             const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float4 w = wc[4 * h2 + e];
-              a[r][0] = fmaf(xs[e], w.x, a[r][0]);
-              a[r][1] = fmaf(xs[e], w.y, a[r][1]);
-              a[r][2] = fmaf(xs[e], w.z, a[r][2]);
-              a[r][3] = fmaf(xs[e], w.w, a[r][3]);
+              acc[r][0] = ffma2(xs[e], w[4 * h2 + e][0], acc[r][0]);
+              acc[r][1] = ffma2(xs[e], w[4 * h2 + e][1], acc[r][1]);
             }
           }
         }
-        ++q;
-      };
-      for (int j = 0; j < nch; ++j) {
-        if (q & 1) run_chunk(j, wnxt, wcur);
-        else run_chunk(j, wcur, wnxt);
       }
       if (tr && L == 5) g_cl_trace[64 * ti + 41] = clock64();
       if (g_cl_trace_on && cid == 0 && rank == 0 && lane == 0 && ti == 0 && L == 5) g_cl_trace[200 + warp] = clock64();
       // pre-reduce the warp's K parts (lanes l, l + kQuads, ...), then across the 8 warps
+      float a[kR][4];
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        const float2 lo = u64_as_f2(acc[r][0]), hi = u64_as_f2(acc[r][1]);
+        a[r][0] = lo.x; a[r][1] = lo.y; a[r][2] = hi.x; a[r][3] = hi.y;
+      }
 #pragma unroll
       for (int r = 0; r < kR; ++r)
 #pragma unroll
@@ -289,16 +323,16 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
         for (int r = 0; r < kR; ++r)
           *reinterpret_cast<float4*>(&S.part[warp][r][4 * cg]) = make_float4(a[r][0], a[r][1], a[r][2], a[r][3]);
       }
-      __syncthreads();
+      tc::named_bar(1, kThreads);
       if (tr && L == 5) g_cl_trace[64 * ti + 42] = clock64();
       {   // kOut adjacent outputs per thread: 16 rays x kCols columns
         float sv[kOut];
 #pragma unroll
         for (int u = 0; u < kOut; ++u) sv[u] = 0.f;
 #pragma unroll
-        for (int w = 0; w < 8; ++w)
+        for (int w8 = 0; w8 < 8; ++w8)
 #pragma unroll
-          for (int u = 0; u < kOut; ++u) sv[u] += S.part[w][rr][cc2 + u];
+          for (int u = 0; u < kOut; ++u) sv[u] += S.part[w8][rr][cc2 + u];
         float v[kOut];
         float* dst;
         if (L == 0 || L == kLayers - 1) {                         // head (no activation) / tail logits
@@ -316,10 +350,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
         }
         const int lb = layer_count & 1;
 #pragma unroll
-        for (int qq = 0; qq < kC; ++qq) {
-          if constexpr (kOut == 4) st_async_v4(remote(qq, dst), v[0], v[1], v[2], v[3], remote(qq, &S.layer_bar[lb]));
-          else st_async_v2(remote(qq, dst), v[0], v[1], remote(qq, &S.layer_bar[lb]));
-        }
+        for (int qq = 0; qq < kC; ++qq) st_async_v4(remote(qq, dst), v[0], v[1], v[2], v[3], remote(qq, &S.layer_bar[lb]));
       }
       if (tr && L == 5) g_cl_trace[64 * ti + 43] = clock64();
       if (tid == 0) tc::mbar_expect_tx(&S.layer_bar[layer_count & 1], kLayerBytes);
@@ -347,7 +378,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
         finish_ray(m, job, out, S.pix[r], S.obj[r], cb, fb, (double)lg[192], wo, wd);
       }
     }
-    __syncthreads();
+    tc::named_bar(1, kThreads);
     if (tr) g_cl_trace[64 * ti + 40] = clock64();
   }
   tc::cluster_sync();           // no CTA leaves while its stores to peers may be in flight
@@ -380,7 +411,7 @@ cudaError_t launch_mlp_fp32_cluster(const GroupTable& gt, const ListSet& ls, con
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kC * (n_sms / kC), 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.blockDim = dim3(kBlock, 1, 1);
     cfg.dynamicSmemBytes = smem;
     int n = 0;
     e = cudaOccupancyMaxActiveClusters(&n, mlp_fp32_cluster_kernel, &cfg);
@@ -388,18 +419,20 @@ cudaError_t launch_mlp_fp32_cluster(const GroupTable& gt, const ListSet& ls, con
     max_clusters = n > 0 ? n : 1;
     if (getenv("NEDF_VERBOSE")) fprintf(stderr, "nedf: fp32 cluster kernel, %d co-resident clusters\n", n);
   }
-  mlp_fp32_cluster_kernel<<<kC * max_clusters, kThreads, smem, stream>>>(gt, ls, job, out);
+  mlp_fp32_cluster_kernel<<<kC * max_clusters, kBlock, smem, stream>>>(gt, ls, job, out);
   return cudaGetLastError();
 }
 
-// Cluster image: layer L, CTA r, thread t (column quad cg = t & 7, K part
-// kp = 4 (t >> 5) + ((t >> 3) & 3)), chunk j -> 32 floats: float4 i =
-// W[c0 .. c0 + 3][k] for K row k = kp * 8 n + 8 j + i (n = chunks of the layer:
-// 4 for the head, 1 after) and c0 = 32 r + 4 cg (head rows are the 16 points'
-// 63 features + 1 zero; tail outputs: fine 0-127, coarse 128-191, alpha 192).
+// Cluster image, streamed as 32 KB stages: stage q (head chunk q < 8, then layer
+// L = 1 + (q - 8) / 2, chunk j = (q - 8) % 2), CTA r -> float4 [(q kC + r) 2048 +
+// 256 i + t] = W[c0 .. c0 + 3][k] for compute thread t (column quad cg = t & 15,
+// K part kp = 2 (t >> 5) + ((t >> 4) & 1)), K row k = kp * 8 n + 8 j + i (n =
+// chunks of the layer: 8 for the head, 2 after) and c0 = 64 r + 4 cg (head rows
+// are the 16 points' 63 features + 1 zero; tail outputs: fine 0-127, coarse
+// 128-191, alpha 192).  Thread-minor float4s make each ring read conflict-free.
 cudaError_t fp32_pack_cluster(const float* P, int d_in, int F, int n_blocks, int n_coarse, int n_fine, float** dev) {
   if (F != 256 || n_blocks != 16 || d_in != kDin || n_coarse != 64 || n_fine != 128) return cudaErrorInvalidValue;
-  std::vector<float> img(kHeadFloats + 33 * kLayerFloats, 0.f);
+  std::vector<float> img(kImageFloats, 0.f);
   size_t p = 0;
   const float* Wh = P + p; p += (size_t)F * d_in + F;
   std::vector<const float*> Wl(32);
@@ -416,19 +449,18 @@ cudaError_t fp32_pack_cluster(const float* P, int d_in, int F, int n_blocks, int
     if (o < 128 + n_coarse + 1) return Wa[(size_t)(o - 128) * F + k];
     return 0.f;
   };
-  for (int L = 0; L < kLayers; ++L) {
+  for (int q = 0; q < kStagesPerTile; ++q) {
+    const int L = q < kHeadChunks ? 0 : 1 + (q - kHeadChunks) / kBodyChunks;
+    const int j = q < kHeadChunks ? q : (q - kHeadChunks) % kBodyChunks;
     const int nch = L == 0 ? kHeadChunks : kBodyChunks;
-    float* base = img.data() + (L == 0 ? 0 : kHeadFloats + (size_t)(L - 1) * kLayerFloats);
     for (int r = 0; r < kC; ++r)
       for (int t = 0; t < kThreads; ++t) {
         const int lane = t & 31, cg = lane % kQuads, kp = kLanesK * (t >> 5) + lane / kQuads;
         const int c0 = kCols * r + 4 * cg;
-        for (int j = 0; j < nch; ++j) {
-          float* dst = base + (((size_t)r * kThreads + t) * nch + j) * kChunk;
-          for (int i = 0; i < 8; ++i) {
-            const int k = kp * 8 * nch + 8 * j + i;
-            for (int u = 0; u < 4; ++u) dst[4 * i + u] = w_of(L, c0 + u, k);
-          }
+        for (int i = 0; i < 8; ++i) {
+          float* dst = img.data() + 4 * (((size_t)q * kC + r) * (kStageBytes / 16) + (size_t)kThreads * i + t);
+          const int k = kp * 8 * nch + 8 * j + i;
+          for (int u = 0; u < 4; ++u) dst[u] = w_of(L, c0 + u, k);
         }
       }
   }
