@@ -96,39 +96,64 @@ __device__ __forceinline__ void top2_push(float v, int col, float& best, float& 
   best = up ? v : best;
 }
 
-// Features of one sample coordinate for the fp16 tensor-core path:
-// [p, sin(2^k pi p), cos(2^k pi p)] k = 0..9.  Bases at k = 0 and 5 use the
-// exactly reduced argument (p split into float hi + lo; 2^k p mod 2 is exact
-// for the hi part), then four double-angle steps each; max abs error ~5e-6,
-// well below the fp16 rounding (2.4e-4 at |v| in [0.5, 1)) that follows.
-__device__ __forceinline__ void encode_coord_tc(double p, float out[21]) {
-  const float ph = (float)p;
-  const float pl = (float)(p - (double)ph);
-  out[0] = ph;
+// Features of one sample point for the fp16 tensor-core path, per coordinate
+// [p, sin(2^k pi p), cos(2^k pi p)] k = 0..9 at f[21 axis ..].  Bases at k = 0
+// and 5 use the exactly reduced argument (p split into float hi + lo; 2^k p
+// mod 2 is exact for the hi part), then four double-angle steps each; max abs
+// error ~5e-6, well below the fp16 rounding (2.4e-4 at |v| in [0.5, 1)) that
+// follows.  Per axis the two recurrences (bases 0 and 5) run as one f32x2
+// chain (FMUL2/FADD2: the same rn operations as scalar code, half the issue slots).
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t add_f2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t sub_f2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul_f2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ void encode_point_tc(const double p[3], float f[64]) {
 #pragma unroll
-  for (int base = 0; base < kLevels; base += 5) {
-    float r;
-    if (base == 0) {
-      r = ph + pl;
-    } else {
-      const float t = ph * 32.0f;                       // exact
-      r = fmaf(-2.0f, rintf(0.5f * t), t) + 32.0f * pl;  // exact reduction + tail
-    }
-    float s, c;
-    __sincosf(3.14159265358979f * r, &s, &c);
-    out[1 + 2 * base] = s;
-    out[2 + 2 * base] = c;
+  for (int ax = 0; ax < 3; ++ax) {
+    const float ph = (float)p[ax];
+    const float pl = (float)(p[ax] - (double)ph);
+    f[21 * ax] = ph;
+    float s0, c0, s5, c5;
+    __sincosf(3.14159265358979f * (ph + pl), &s0, &c0);
+    const float t = ph * 32.0f;                                          // exact
+    __sincosf(3.14159265358979f * (fmaf(-2.0f, rintf(0.5f * t), t) + 32.0f * pl), &s5, &c5);   // exact reduction + tail
+    f[21 * ax + 1] = s0;
+    f[21 * ax + 2] = c0;
+    f[21 * ax + 11] = s5;
+    f[21 * ax + 12] = c5;
+    uint64_t S = f2pack(s0, s5), C = f2pack(c0, c5);     // lanes: level k, level 5 + k
 #pragma unroll
-    for (int k = base + 1; k < base + 5; ++k) {
-      const float s2 = 2.0f * s * c;
-      const float c2 = (c - s) * (c + s);
-      s = s2;
-      c = c2;
-      out[1 + 2 * k] = s;
-      out[2 + 2 * k] = c;
+    for (int k = 1; k < 5; ++k) {
+      const uint64_t sc = mul_f2(S, C);
+      const uint64_t S2 = add_f2(sc, sc);                 // 2 s c (exact doubling)
+      C = mul_f2(sub_f2(C, S), add_f2(C, S));             // (c - s)(c + s)
+      S = S2;
+      f2unpack(S, f[21 * ax + 1 + 2 * k], f[21 * ax + 11 + 2 * k]);
+      f2unpack(C, f[21 * ax + 2 + 2 * k], f[21 * ax + 12 + 2 * k]);
     }
   }
+  f[63] = 0.f;
 }
+
 
 }  // namespace
 
@@ -364,20 +389,15 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
         if (valid) {
           const double tt = t0 + (t1 - t0) * lin16(pt);
           float f[64];
-#pragma unroll
-          for (int ax = 0; ax < 3; ++ax) {
-            float e[21];
-            encode_coord_tc(pa[ax] + tt * pb[ax], e);
-#pragma unroll
-            for (int j = 0; j < 21; ++j) f[21 * ax + j] = e[j];
-          }
-          f[63] = 0.f;
+          const double pp[3] = {pa[0] + tt * pb[0], pa[1] + tt * pb[1], pa[2] + tt * pb[2]};
+          encode_point_tc(pp, f);
 #pragma unroll
           for (int j = 0; j < 32; ++j) packed[j] = tc::pack_h2(f[2 * j], f[2 * j + 1]);
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) packed[j] = 0u;
         }
+        trace_at(tr, 500 + pt);
         // A_Q is free for this tile's points once the previous tile's layer 32 completed; within the
         // tile, slot pt & 3 is free once point pt - 4 was consumed
         if (pt == 0 && ti > 0) tc::mbar_wait(&S.aq_free, (ti - 1) & 1);

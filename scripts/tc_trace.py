@@ -17,7 +17,8 @@ tr = lib.nedf_diag_tc_trace
 tr.restype = C.c_int
 tr.argtypes = [C.c_int, C.POINTER(C.c_ulonglong), C.c_int]
 
-_lib.context().set_option(_lib.OPT_TC_KERNEL, _lib.TC_SINGLE)
+# tc kernel variant (argv[2]): 1 single CTA (default), 3 cluster-multicast pair, 4 multicast x4
+_lib.context().set_option(_lib.OPT_TC_KERNEL, int(sys.argv[2]) if len(sys.argv) > 2 else _lib.TC_SINGLE)
 spec = CF.config4()
 scene, cam, lights, cfg = scenes.build(spec)
 buf = pipeline.FrameBuffers(cam.width, cam.height)
@@ -33,6 +34,7 @@ t = np.array(out[:], dtype=np.int64)
 t0 = t[0]
 rel = lambda i: int(t[i] - t0) if t[i] else None
 print("producer layer starts:", [rel(450 + L) for L in range(34)])
+print("encoder point computed:     ", [rel(500 + p) for p in range(16)])
 print("encoder point slot acquired:", [rel(420 + p) for p in range(16)])
 print("encoder point written:      ", [rel(400 + p) for p in range(16)])
 prev_end = None
