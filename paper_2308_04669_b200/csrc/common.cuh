@@ -63,16 +63,22 @@ struct DevObj {
 // ray (o + t d, t >= 0) certainly misses the sphere (centre c, radius r)
 // -- the margin covers fp32 rounding of coordinates up to ~1e4 with room to spare,
 // so the exact clip still decides every pair that could hit.
-__device__ __forceinline__ bool sphere_miss(const DevObj& ob, const double o[3], const double d[3]) {
-  const float wx = ob.bs_c[0] - (float)o[0], wy = ob.bs_c[1] - (float)o[1], wz = ob.bs_c[2] - (float)o[2];
-  const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
+// (c, r1 = 1.001 r) as staged by the setup kernel; o, d already rounded to fp32.
+// Division-free: for t >= 0 the line misses iff (|w|^2 - r^2) |d|^2 > (w.d)^2.
+__device__ __forceinline__ bool sphere_miss_f(float4 cr, float ox, float oy, float oz, float dx, float dy, float dz) {
+  const float wx = cr.x - ox, wy = cr.y - oy, wz = cr.z - oz;
   const float w2 = wx * wx + wy * wy + wz * wz;
   const float tca = wx * dx + wy * dy + wz * dz;
-  const float r = ob.bs_r * 1.001f + 1e-3f * (1.0f + sqrtf(w2));
-  if (w2 <= r * r) return false;             // origin inside (or near) the sphere: no decision
+  const float r = cr.w + 1e-3f * (1.0f + sqrtf(w2));
+  const float e = w2 - r * r;
+  if (e <= 0.f) return false;                // origin inside (or near) the sphere: no decision
   if (tca < 0.f) return true;                // sphere behind the origin
   const float dd = dx * dx + dy * dy + dz * dz;
-  return w2 - tca * tca / dd > r * r;        // the line passes outside
+  return e * dd > tca * tca;                 // the line passes outside
+}
+__device__ __forceinline__ bool sphere_miss(const DevObj& ob, const double o[3], const double d[3]) {
+  return sphere_miss_f(make_float4(ob.bs_c[0], ob.bs_c[1], ob.bs_c[2], ob.bs_r * 1.001f), (float)o[0], (float)o[1],
+                       (float)o[2], (float)d[0], (float)d[1], (float)d[2]);
 }
 
 struct DevCam {

@@ -37,8 +37,21 @@ __device__ __forceinline__ bool analytic_depth(const FrameJob& fj, const DevObj&
 }
 
 // Enqueue the (ray, object) pairs that reach the network and trace analytic
-// objects.  mode: RAY_PRIMARY (STEP 1) or a shadow mode (STEP 3).
-__global__ void setup_kernel(FrameJob fj, GroupTable gt, ListSet ls, int mode) {
+// objects.  mode: RAY_PRIMARY (STEP 1) or a shadow mode (STEP 3).  The first
+// kSetupStage objects' prefilter data (bounding sphere, kind, flags) is staged
+// in shared memory once per block; the pixel loop then touches an object's
+// full descriptor only when its fp32 sphere test passes.
+constexpr int kSetupStage = 64;
+__global__ void __launch_bounds__(256, 4) setup_kernel(FrameJob fj, GroupTable gt, ListSet ls, int mode) {
+  __shared__ float4 s_sph[kSetupStage];
+  __shared__ int s_flags[kSetupStage];      // bit 0: NeDF, bit 1: plane kept from the cache (skip)
+  const bool cached = mode == RAY_PRIMARY && fj.planes != nullptr;
+  for (int s = threadIdx.x; s < fj.n_objs && s < kSetupStage; s += blockDim.x) {
+    const DevObj& ob = fj.ray.objs[s];
+    s_sph[s] = make_float4(ob.bs_c[0], ob.bs_c[1], ob.bs_c[2], ob.bs_r * 1.001f);
+    s_flags[s] = (ob.depth_kind == NEDF_DEPTH_NEDF ? 1 : 0) | (cached && !ob.recompute ? 2 : 0);
+  }
+  __syncthreads();
   const int stride = gridDim.x * blockDim.x;
   for (int base = blockIdx.x * blockDim.x; base < fj.n_pix; base += stride) {
     const int p = base + threadIdx.x;
@@ -49,22 +62,34 @@ __global__ void setup_kernel(FrameJob fj, GroupTable gt, ListSet ls, int mode) {
     }
     double o[3] = {0, 0, 0}, d[3] = {0, 0, 1};
     if (live) item_world_ray(fj.ray, (uint32_t)p, o, d);
+    const float ox = (float)o[0], oy = (float)o[1], oz = (float)o[2];
+    const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
     unsigned long long key = kEmptyKey;
     for (int s = 0; s < fj.n_objs; ++s) {
-      const DevObj& ob = fj.ray.objs[s];
-      if (mode == RAY_PRIMARY && fj.planes != nullptr && !ob.recompute) continue;   // cached plane kept
-      if (ob.depth_kind == NEDF_DEPTH_NEDF) {
+      int flags;
+      float4 sph;
+      if (s < kSetupStage) {
+        flags = s_flags[s];
+        sph = s_sph[s];
+      } else {
+        const DevObj& ob = fj.ray.objs[s];
+        flags = (ob.depth_kind == NEDF_DEPTH_NEDF ? 1 : 0) | (cached && !ob.recompute ? 2 : 0);
+        sph = make_float4(ob.bs_c[0], ob.bs_c[1], ob.bs_c[2], ob.bs_r * 1.001f);
+      }
+      if (flags & 2) continue;                                                       // cached plane kept
+      if (flags & 1) {
         bool hit = false;
-        if (live && !sphere_miss(ob, o, d)) {
+        if (live && !sphere_miss_f(sph, ox, oy, oz, dx, dy, dz)) {
+          const DevObj& ob = fj.ray.objs[s];
           const DevModel& m = gt.models[ob.group];
           double lo[3], ld[3], t0, t1;
           to_local(ob, o, d, lo, ld);
           hit = slab_clip(lo, ld, m.bmin, m.bmax, t0, t1);
         }
-        warp_append(ls, ob.group, hit, (uint32_t)p, (uint32_t)s);
-        if (mode == RAY_PRIMARY && fj.planes != nullptr && p < fj.n_pix)
-          fj.planes[(size_t)s * fj.n_pix + p] = INFINITY;
+        if (__any_sync(0xffffffffu, hit)) warp_append(ls, fj.ray.objs[s].group, hit, (uint32_t)p, (uint32_t)s);
+        if (cached && p < fj.n_pix) fj.planes[(size_t)s * fj.n_pix + p] = INFINITY;
       } else if (live) {
+        const DevObj& ob = fj.ray.objs[s];
         double dep;
         bool hit = analytic_depth(fj, ob, o, d, dep);
         // directional shadows accept depth-0 hits (pipeline.py:362-364)
@@ -73,8 +98,8 @@ __global__ void setup_kernel(FrameJob fj, GroupTable gt, ListSet ls, int mode) {
           unsigned long long k = pack_key(dep, (uint32_t)s, 0, 0);
           key = k < key ? k : key;
         }
-        if (mode == RAY_PRIMARY && fj.planes != nullptr) fj.planes[(size_t)s * fj.n_pix + p] = ok ? dep : INFINITY;
-      } else if (mode == RAY_PRIMARY && fj.planes != nullptr && p < fj.n_pix) {
+        if (cached) fj.planes[(size_t)s * fj.n_pix + p] = ok ? dep : INFINITY;
+      } else if (cached && p < fj.n_pix) {
         fj.planes[(size_t)s * fj.n_pix + p] = INFINITY;
       }
     }
