@@ -49,7 +49,7 @@ constexpr int kLanesK = 32 / kQuads;  // K parts per warp
 constexpr int kThreads = 256;         // compute threads: kKP K parts x kQuads column quads
 constexpr int kBlock = kThreads + 32; // + the weight producer warp
 constexpr int kKP = 8 * kLanesK;      // K parts (8 warps)
-constexpr int kR = 16;                // rays per cluster tile
+constexpr int kRMax = 16;             // rays per cluster tile: 8, 12 or 16, the smallest that fits one round
 constexpr int kHeadK = 1024;          // 16 points x (63 features + 1 zero)
 constexpr int kChunk = 32;            // weights per thread per chunk: 8 K rows x 4 columns
 constexpr int kHeadChunks = kHeadK / kKP / 8;   // 8-row chunks per thread: head (8)
@@ -61,20 +61,18 @@ constexpr int kRing = 3;
 constexpr size_t kImageFloats = (size_t)kStagesPerTile * kC * kThreads * kChunk;
 
 struct ClSmem {
-  float4 ring[kRing][kStageBytes / 16];   // stage slot: float4 i of thread t at [8 i... see fp32_pack_cluster]
-  float f[kR][kHeadK];
-  float x[kR][256];
-  float h[kR][256];
-  float part[8][kR][kCols];      // per warp (its K parts pre-reduced by shuffle)
-  double ray[kR][8];
-  uint32_t pix[kR], obj[kR];
-  int valid[kR];
+  float4 ring[kRing][kStageBytes / 16];   // weight stage slots: float4 i of compute thread t at [256 i + t]
+  float f[kRMax][kHeadK];
+  float x[kRMax][256];
+  float h[kRMax][256];
+  float part[8][kRMax][kCols];   // per warp (its K parts pre-reduced by shuffle)
+  double ray[kRMax][8];
+  uint32_t pix[kRMax], obj[kRMax];
+  int valid[kRMax];
   uint64_t full[kRing], empty[kRing];
   uint64_t feat_bar;             // features of the tile: 64 KB from the 4 CTAs
   uint64_t layer_bar[2];         // layer L outputs (16 KB from the 4 CTAs) on layer_bar[L & 1]
 };
-constexpr uint32_t kFeatBytes = kR * kHeadK * 4;
-constexpr uint32_t kLayerBytes = kR * 256 * 4;
 
 // remote store that completes its bytes on the receiving CTA's mbarrier
 __device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uint32_t mbar) {
@@ -118,56 +116,14 @@ __device__ __forceinline__ float2 u64_as_f2(uint64_t v) {
 __device__ unsigned long long g_cl_trace[256];
 __device__ int g_cl_trace_on;
 
-__global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kBlock, 1)
-mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  ClSmem& S = *reinterpret_cast<ClSmem*>(smem_raw);
-  __shared__ int s_tiles[65];
+// The compute warps' tile loop for R-ray tiles (R = 8, 12, 16).
+template <int R>
+__device__ __forceinline__ void guard_tiles(ClSmem& S, const int* s_tiles, int total, int ng, const GroupTable& gt,
+                                            const ListSet& ls, const RayJob& job, const OutSpec& out, uint32_t rank,
+                                            int cid, int n_cl) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const uint32_t rank = tc::cluster_rank();
-  const int cid = blockIdx.x / kC, n_cl = gridDim.x / kC;
-  const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
   const bool feats_in = out.feats != nullptr;
-
-  if (tid == 0) {
-    int cum = 0;
-    s_tiles[0] = 0;
-    for (int g = 0; g < ng; ++g) {
-      cum += (ls.count[g] + kR - 1) / kR;
-      s_tiles[g + 1] = cum;
-    }
-    for (int i = 0; i < kRing; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], 8); }
-    tc::mbar_init(&S.feat_bar, 1);
-    tc::mbar_init(&S.layer_bar[0], 1);
-    tc::mbar_init(&S.layer_bar[1], 1);
-    tc::mbar_fence_init();
-  }
-  tc::cluster_sync();           // peers' barriers initialised before anyone stores into them
-  const int total = s_tiles[ng];
-
-  if (warp == 8) {
-    // ---------------------------------------------------------------- weight producer
-    // stage q of a tile = this CTA's 32 KB slice of (head chunk q | layer 1 + (q - 8) / 2, chunk (q - 8) % 2)
-    if (lane == 0) {
-      uint32_t gq = 0;
-      for (int t = cid; t < total; t += n_cl) {
-        int g = 0;
-        while (g < ng - 1 && t >= s_tiles[g + 1]) ++g;
-        const unsigned char* img = reinterpret_cast<const unsigned char*>(gt.models[g].wcluster);
-        for (int q = 0; q < kStagesPerTile; ++q, ++gq) {
-          const int slot = gq % kRing;
-          tc::mbar_wait(&S.empty[slot], ((gq / kRing) & 1) ^ 1);
-          tc::mbar_expect_tx(&S.full[slot], kStageBytes);
-          tc::bulk_g2s(&S.ring[slot][0], img + ((size_t)q * kC + rank) * kStageBytes, kStageBytes, &S.full[slot]);
-        }
-      }
-    }
-    __syncwarp();
-    tc::cluster_sync();
-    return;
-  }
-
   // ------------------------------------------------------------------ compute warps
   const int cg = lane % kQuads, kp = kLanesK * warp + lane / kQuads;
   // shared::cluster address of S in every CTA of the cluster
@@ -184,11 +140,11 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
     int g = 0;
     while (g < ng - 1 && t >= s_tiles[g + 1]) ++g;
     const int lt = t - s_tiles[g];
-    int n = ls.count[g] - lt * kR;
-    n = n < kR ? n : kR;
-    const int64_t base = ls.offset[g] + (int64_t)lt * kR;
+    int n = ls.count[g] - lt * R;
+    n = n < R ? n : R;
+    const int64_t base = ls.offset[g] + (int64_t)lt * R;
     const DevModel& m = gt.models[g];
-    if (tid < kR) {
+    if (tid < R) {
       const int r = tid;
       const int v = r < n;
       S.valid[r] = v;
@@ -211,7 +167,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
     // ---- head features: this CTA computes sample points kPtsPerCta rank .. kPtsPerCta (rank + 1) - 1 and broadcasts them
     // (float64, geometry.py:312-342); one (ray, point, coordinate, level) per thread
     constexpr int kPtsPerCta = kPoints / kC;
-    for (int e = tid; e < kR * kPtsPerCta * 33; e += kThreads) {
+    for (int e = tid; e < R * kPtsPerCta * 33; e += kThreads) {
       const int r = e / (kPtsPerCta * 33), rem = e % (kPtsPerCta * 33), p2 = rem / 33, a = (rem / 11) % 3,
                 lev = rem % 11;
       const int pt = kPtsPerCta * (int)rank + p2;
@@ -248,7 +204,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
         }
       }
     }
-    if (tid == 0) tc::mbar_expect_tx(&S.feat_bar, kFeatBytes);
+    if (tid == 0) tc::mbar_expect_tx(&S.feat_bar, (uint32_t)(R * kHeadK * 4));
     tc::mbar_wait(&S.feat_bar, feat_phase);
     feat_phase ^= 1;
     if (tr) g_cl_trace[64 * ti + 2] = clock64();
@@ -270,9 +226,9 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
 #pragma unroll
         for (int u = 0; u < kOut; ++u) bnext[u] = __ldg(bias_p + (L + 1) * 256 + col2 + u);
       }
-      uint64_t acc[kR][2];                           // columns (4 cg, 4 cg + 1), (4 cg + 2, 4 cg + 3)
+      uint64_t acc[R][2];                           // columns (4 cg, 4 cg + 1), (4 cg + 2, 4 cg + 3)
 #pragma unroll
-      for (int r = 0; r < kR; ++r) acc[r][0] = acc[r][1] = 0ull;
+      for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = 0ull;
       for (int j = 0; j < nch; ++j) {
         // this chunk's weights: float4 i = W[c0 .. c0 + 3][k0 + i], copied out of the ring slot, which is
         // then released to the producer before the FMAs
@@ -292,7 +248,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
 #pragma unroll
-          for (int r = 0; r < kR; ++r) {
+          for (int r = 0; r < R; ++r) {
             const float4 x4 = *reinterpret_cast<const float4*>(inp + r * ld_in + 4 * h2);
             const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
@@ -306,26 +262,26 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       if (tr && L == 5) g_cl_trace[64 * ti + 41] = clock64();
       if (g_cl_trace_on && cid == 0 && rank == 0 && lane == 0 && ti == 0 && L == 5) g_cl_trace[200 + warp] = clock64();
       // pre-reduce the warp's K parts (lanes l, l + kQuads, ...), then across the 8 warps
-      float a[kR][4];
+      float a[R][4];
 #pragma unroll
-      for (int r = 0; r < kR; ++r) {
+      for (int r = 0; r < R; ++r) {
         const float2 lo = u64_as_f2(acc[r][0]), hi = u64_as_f2(acc[r][1]);
         a[r][0] = lo.x; a[r][1] = lo.y; a[r][2] = hi.x; a[r][3] = hi.y;
       }
 #pragma unroll
-      for (int r = 0; r < kR; ++r)
+      for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
           for (int off = kQuads; off < 32; off <<= 1) a[r][u] += __shfl_xor_sync(0xffffffffu, a[r][u], off);
       if (lane < kQuads) {
 #pragma unroll
-        for (int r = 0; r < kR; ++r)
+        for (int r = 0; r < R; ++r)
           *reinterpret_cast<float4*>(&S.part[warp][r][4 * cg]) = make_float4(a[r][0], a[r][1], a[r][2], a[r][3]);
       }
       tc::named_bar(1, kThreads);
       if (tr && L == 5) g_cl_trace[64 * ti + 42] = clock64();
-      {   // kOut adjacent outputs per thread: 16 rays x kCols columns
+      if (rr < R) {   // kOut adjacent outputs per thread: R rays x kCols columns
         float sv[kOut];
 #pragma unroll
         for (int u = 0; u < kOut; ++u) sv[u] = 0.f;
@@ -353,13 +309,13 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
         for (int qq = 0; qq < kC; ++qq) st_async_v4(remote(qq, dst), v[0], v[1], v[2], v[3], remote(qq, &S.layer_bar[lb]));
       }
       if (tr && L == 5) g_cl_trace[64 * ti + 43] = clock64();
-      if (tid == 0) tc::mbar_expect_tx(&S.layer_bar[layer_count & 1], kLayerBytes);
+      if (tid == 0) tc::mbar_expect_tx(&S.layer_bar[layer_count & 1], (uint32_t)(R * 256 * 4));
       tc::mbar_wait(&S.layer_bar[layer_count & 1], (layer_count >> 1) & 1);
       ++layer_count;
       if (tr) g_cl_trace[64 * ti + 3 + L] = clock64();
     }
     // ---- decode: fine = logits[0:128), coarse = [128:192), alpha = [192] (model.py:277-293)
-    if (rank == 0 && tid < kR && S.valid[tid]) {
+    if (rank == 0 && tid < R && S.valid[tid]) {
       const int r = tid;
       const float* lg = S.h[r];
       if (out.mode == OUT_LOGITS) {
@@ -381,6 +337,71 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
     tc::named_bar(1, kThreads);
     if (tr) g_cl_trace[64 * ti + 40] = clock64();
   }
+}
+
+__global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kBlock, 1)
+mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  ClSmem& S = *reinterpret_cast<ClSmem*>(smem_raw);
+  __shared__ int s_tiles[65];
+  __shared__ int s_R;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = tc::cluster_rank();
+  const int cid = blockIdx.x / kC, n_cl = gridDim.x / kC;
+  const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
+
+  if (tid == 0) {
+    // tile size: the smallest of 8, 12, 16 rays whose tiles all run in one round of clusters (the
+    // per-layer FMA time scales with the rays per tile, the exchange latency does not)
+    int R = 16;
+    for (int cand = 8; cand < 16; cand += 4) {
+      int tiles = 0;
+      for (int g = 0; g < ng; ++g) tiles += (ls.count[g] + cand - 1) / cand;
+      if (tiles <= n_cl) { R = cand; break; }
+    }
+    s_R = R;
+    int cum = 0;
+    s_tiles[0] = 0;
+    for (int g = 0; g < ng; ++g) {
+      cum += (ls.count[g] + R - 1) / R;
+      s_tiles[g + 1] = cum;
+    }
+    for (int i = 0; i < kRing; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], 8); }
+    tc::mbar_init(&S.feat_bar, 1);
+    tc::mbar_init(&S.layer_bar[0], 1);
+    tc::mbar_init(&S.layer_bar[1], 1);
+    tc::mbar_fence_init();
+  }
+  tc::cluster_sync();           // peers' barriers initialised before anyone stores into them
+  const int total = s_tiles[ng];
+
+  if (warp == 8) {
+    // ---------------------------------------------------------------- weight producer
+    // stage q of a tile = this CTA's 32 KB slice of (head chunk q | layer 1 + (q - 8) / 2, chunk (q - 8) % 2)
+    if (lane == 0) {
+      uint32_t gq = 0;
+      for (int t = cid; t < total; t += n_cl) {
+        int g = 0;
+        while (g < ng - 1 && t >= s_tiles[g + 1]) ++g;
+        const unsigned char* img = reinterpret_cast<const unsigned char*>(gt.models[g].wcluster);
+        for (int q = 0; q < kStagesPerTile; ++q, ++gq) {
+          const int slot = gq % kRing;
+          tc::mbar_wait(&S.empty[slot], ((gq / kRing) & 1) ^ 1);
+          tc::mbar_expect_tx(&S.full[slot], kStageBytes);
+          tc::bulk_g2s(&S.ring[slot][0], img + ((size_t)q * kC + rank) * kStageBytes, kStageBytes, &S.full[slot]);
+        }
+      }
+    }
+    __syncwarp();
+    tc::cluster_sync();
+    return;
+  }
+
+  // ------------------------------------------------------------------ compute warps
+  if (s_R == 8) guard_tiles<8>(S, s_tiles, total, ng, gt, ls, job, out, rank, cid, n_cl);
+  else if (s_R == 12) guard_tiles<12>(S, s_tiles, total, ng, gt, ls, job, out, rank, cid, n_cl);
+  else guard_tiles<16>(S, s_tiles, total, ng, gt, ls, job, out, rank, cid, n_cl);
   tc::cluster_sync();           // no CTA leaves while its stores to peers may be in flight
 }
 
