@@ -54,7 +54,7 @@ def parse():
 
 def traffic_per_launch():
     """dram__bytes_read.sum + dram__bytes_write.sum of one network launch from the committed
-    ncu --set full capture (profiles/r1_tc_kernel_ncu.json), or None."""
+    ncu capture of the benchmarked kernel (profiles/r1_tc_kernel_ncu.json), or None."""
     f = ROOT / "profiles" / "r1_tc_kernel_ncu.json"
     try:
         return json.loads(f.read_text())["dram_bytes_per_launch"]
@@ -317,7 +317,7 @@ def main():
                 if ctx.get_option(_lib.OPT_PRECISION) != _lib.PREC_FP32 else "mlp_fp32_stream_kernel",
                 "kernel_ms_per_frame": net_ms, "guard_ms_per_frame": guard_ms,
                 "flop_per_eval": FLOP_PER_EVAL, "evals_per_launch": evals / max(1, st["net_launches"] / args.steps),
-                "traffic": traffic_per_launch(), "traffic_unit": "bytes (DRAM read + write per launch, ncu --set full)"}
+                "traffic": traffic_per_launch(), "traffic_unit": "bytes (DRAM read + write per launch, ncu)"}
     line = {
         "metric": METRIC, "value": t_frame, "unit": "ms/frame", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": t_frame, "higher_is_better": False, "scaling": "strong",

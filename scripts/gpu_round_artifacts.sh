@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round artifacts on one GPU: headline bench (both arms), the other §8 workloads, the ncu launch
-# list of the bench command and full captures of the network and guard kernels.
+# list of the bench command, and ncu captures of the network and guard kernels.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout 300 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -1 gpurun_out/bench.json
@@ -9,7 +9,15 @@ timeout 400 python scripts/bench_configs.py --out gpurun_out/configs.jsonl > /de
 # launch list of the same command (cold-cache, serialised per-launch times)
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launches.log 2>&1; echo launches rc=$?
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:nedf_mlp_tc_kernel -s 2 -c 1 \
+# network kernel as benchmarked (cluster-multicast pair): counters only -- the full set's source-level
+# instrumentation hangs the multicast cluster kernel; the full set with source is taken on the
+# single-CTA variant (same MMA / epilogue / encoder code, no multicast)
+M=gpu__time_duration.sum,sm__cycles_elapsed.avg,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_elapsed,lts__throughput.avg.pct_of_peak_sustained_elapsed,l1tex__m_xbar2l1tex_read_bytes.sum,launch__registers_per_thread,launch__grid_size,launch__block_size,launch__shared_mem_per_block_dynamic,launch__cluster_dim_x,sm__throughput.avg.pct_of_peak_sustained_elapsed
+timeout 300 ncu --metrics $M --clock-control none -k regex:nedf_mlp_tc_kernel -s 2 -c 1 \
   -o gpurun_out/tc_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_tc.log 2>&1; echo tc rc=$?
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:nedf_mlp_tc_kernel -s 2 -c 1 \
+  -o gpurun_out/tc_single_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --tc-kernel single > gpurun_out/ncu_tc_single.log 2>&1; echo tc single rc=$?
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:mlp_fp32_cluster -s 2 -c 1 \
   -o gpurun_out/guard_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_guard.log 2>&1; echo guard rc=$?
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:setup_kernel -s 2 -c 1 \
+  -o gpurun_out/setup_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_setup.log 2>&1; echo setup rc=$?

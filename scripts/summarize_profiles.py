@@ -83,12 +83,17 @@ def main():
                            "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e")
         (dst / f"{p}_launches_config4_summary.json").write_text(json.dumps(s, indent=1) + "\n")
         shutil.copy(src / "launches.csv", dst / f"{p}_launches_config4.csv")
-    for rep, kern, regex, out in [("guard_full.ncu-rep", "mlp_fp32_cluster_kernel", "mlp_fp32_cluster", "guard"),
-                                  ("tc_full.ncu-rep", "nedf_mlp_tc_kernel", "nedf_mlp_tc_kernel", "tc")]:
+    base = "python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+    for rep, kern, cap, out in [
+            ("guard_full.ncu-rep", "mlp_fp32_cluster_kernel", "--set full -k regex:mlp_fp32_cluster", "guard"),
+            ("tc_full.ncu-rep", "nedf_mlp_tc_kernel (cluster-multicast pair, as benchmarked)",
+             "--metrics <list in scripts/gpu_round_artifacts.sh> -k regex:nedf_mlp_tc_kernel", "tc"),
+            ("tc_single_full.ncu-rep", "nedf_mlp_tc_kernel (single-CTA variant)",
+             "--set full -k regex:nedf_mlp_tc_kernel [--tc-kernel single]", "tc_single_full"),
+            ("setup_full.ncu-rep", "setup_kernel", "--set full -k regex:setup_kernel", "setup")]:
         if (src / rep).exists() and (src / rep).stat().st_size > 0:
             try:
-                s = rep_summary(src / rep, kern, f"ncu --set full --clock-control none -k regex:{regex} -s 2 -c 1 "
-                                "python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e",
+                s = rep_summary(src / rep, kern, f"ncu {cap} --clock-control none -s 2 -c 1 {base}",
                                 "STEP-1 launch of a config-4 frame")
                 (dst / f"{p}_{out}_kernel_ncu.json").write_text(json.dumps(s, indent=1) + "\n")
             except (subprocess.CalledProcessError, IndexError) as e:
