@@ -173,15 +173,18 @@ def test_frames_are_deterministic(P):
     np.testing.assert_array_equal(i1, r2.image.cpu().numpy())
 
 
-def test_cluster_guard_kernel_matches_fp32_path(P):
+@pytest.mark.parametrize("n_rays", [3000, 300, 60])
+def test_cluster_guard_kernel_matches_fp32_path(P, n_rays):
     """With the guard threshold at 100% of max|logit| every ray is re-evaluated
     by the cluster-split fp32 kernel (mlp_fp32c.cu); its decisions must match
     the streaming fp32 kernel's (NEDF_PREC_FP32) up to fp32 summation-order
-    ties, and its depths must agree to float32 accuracy."""
+    ties, and its depths must agree to float32 accuracy.  The ray counts cover
+    the kernel's tile sizes: 16-ray tiles over several rounds (3000), 12-ray
+    tiles (300) and 8-ray tiles (60) in one round of clusters."""
     _lib, fields, geometry, model, pipeline, scenes = _mods()
     ctx = _lib.context()
     m = scenes.paper_model(1, "box")
-    o, d = CF.sweep_rays(3000, m.relaxed_box.min, m.relaxed_box.max, seed=11)
+    o, d = CF.sweep_rays(n_rays, m.relaxed_box.min, m.relaxed_box.max, seed=11)
     ctx.set_option(_lib.OPT_PRECISION, _lib.PREC_FP32)
     mu32, a32 = model.query_rays(m, o, d)
     ctx.set_option(_lib.OPT_PRECISION, _lib.PREC_AUTO)
@@ -190,10 +193,11 @@ def test_cluster_guard_kernel_matches_fp32_path(P):
         mug, ag = model.query_rays(m, o, d)
     finally:
         ctx.set_option(_lib.OPT_GUARD_PPM, 3000)
-    assert (ag == a32).mean() > 0.999
+    allowed = max(1, n_rays // 1000)        # fp32 summation-order near-ties
+    assert (ag != a32).sum() <= allowed
     fin = np.isfinite(mu32) & np.isfinite(mug)
     same = np.abs(mug[fin] - mu32[fin]) <= 1e-12
-    assert same.mean() > 0.999
+    assert (~same).sum() <= allowed
     # a differing ray differs by one fine bin at most (fp32 near-tie)
     fine = 2 * m.config.half_range / m.n_coarse / m.n_fine
     assert np.all(np.abs(mug[fin] - mu32[fin]) <= fine * 1.0001 + 2 * m.config.half_range / m.n_coarse)
