@@ -1,34 +1,37 @@
-// fp32 network for small ray batches, split across a cluster of kC = 4 CTAs.
+// fp32-accurate network for small ray batches, split across a cluster of
+// kC = 4 CTAs, on the warp-level tensor cores (mma.sync, 3xTF32).
 //
 // Role: the near-tie guard's re-evaluation (a few hundred rays per frame).
 // Its cost is latency, not FLOPs: one ray still walks a 35-layer chain.  The
-// streaming kernel (mlp_fp32s.cu) runs that chain inside one SM, streaming the
-// whole 9.5 MB fp32 weight image through it.  Here the 4 CTAs of a cluster
-// share each ray tile: CTA r owns output columns [64 r, 64 r + 64) of every
-// layer, so it needs only its 1/4 of the weights, and scatters its outputs into
-// every peer's activation buffer with st.async through distributed shared
-// memory.  Each store completes transaction bytes on the receiving CTA's
-// mbarrier, so a CTA starts layer L+1 as soon as all 16 KB of layer L have
-// landed -- no cluster-wide barrier per layer.  Buffer reuse is safe without
-// one: a CTA can only produce layer L+1 after receiving every peer's layer-L
-// outputs, i.e. after every peer finished reading the buffer layer L+1
-// overwrites.  Two layer barriers alternate so a peer one layer ahead never
-// completes the current phase.  Same arithmetic as mlp_fp32s.cu: float64
-// features, float32 weights and accumulation (a different summation order).
+// 4 CTAs of a cluster share a 16-ray tile: CTA r owns output columns
+// [64 r, 64 r + 64) of every layer, so it needs only its 1/4 of the weights,
+// and scatters its outputs into every peer's activation buffer with st.async
+// through distributed shared memory.  Each store completes transaction bytes
+// on the receiving CTA's mbarrier, so a CTA starts layer L+1 as soon as all
+// 16 KB of layer L have landed -- no cluster-wide barrier per layer.  Buffer
+// reuse is safe without one: a warp sends its layer-L outputs only after its
+// layer-L MMAs, so once every layer-L output has landed anywhere, every warp
+// of the cluster is done reading the buffer layer L+1 overwrites.  Two layer
+// barriers alternate so a peer one layer ahead never completes the current
+// phase.
+//
+// Arithmetic: warp w of a CTA owns 8 output columns and the whole K range of
+// every layer, so a layer is 16 rays x 8 columns x K per warp with no
+// cross-warp reduction: m16n8k8 TF32 MMAs with fp32 accumulation, each
+// operand split into a TF32 high part and a TF32 remainder and three products
+// accumulated (a_lo b_hi + a_hi b_lo + a_hi b_hi; the dropped a_lo b_lo term
+// is ~2^-20 of a product), i.e. near-fp32 accuracy on the tensor pipe.  A
+// 16 x 64 x 256 layer slice takes ~3.4k cycles of HMMA (ncu: "math" throttle
+// on the MMA pipe; scripts/cl_trace.py) against ~4.2k for the same slice as
+// FFMA2 (the previous version of this kernel); the split runs on LOP3/FADD,
+// since cvt.rna.tf32 issues at a quarter rate.
+// Float64 features (sincospi), float32 weights and activations.
 //
 // Weights: a producer warp (warp 8) streams the CTA's slice of the image as
-// 32 KB stages (one 8 K-row x 4-column chunk per compute thread; the head is 8
-// stages, every later layer 2) through a 3-slot shared-memory ring with bulk
-// copies, so the compute warps never wait on L2 latency; a compute warp copies
-// its chunk into registers and releases the slot before its FMAs.  The FMAs are
-// FFMA2 (fma.rn.f32x2: one x value times a pair of columns), the same fp32
-// operations in the same order as scalar FMAs, at half the issue slots.
-//
-// Thread layout (256 compute threads): column quad cg = lane & 15 (columns 4 cg
-// .. 4 cg + 3 of the CTA's 64), K part kp = 2 warp + (lane >> 4) of 16 (16 K rows
-// per layer, 64 for the head), so every x value loaded from shared memory feeds
-// 4 FMAs.  Cluster size: 4 CTAs lets ~35 clusters (140 SMs) co-reside, so a
-// frame's guard batch is one round of 16-ray tiles.
+// 32 KB stages (128 K rows x 64 columns; the head is 8 stages, every later
+// layer 2) through a 3-slot shared-memory ring with bulk copies; a compute
+// warp copies its part of a stage into registers and releases the slot
+// before its MMAs.
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -43,36 +46,36 @@ namespace nedf {
 namespace {
 
 constexpr int kC = 4;                 // CTAs per cluster
-constexpr int kCols = 256 / kC;       // output columns per CTA (64)
-constexpr int kQuads = kCols / 4;     // column quads per CTA (one per lane group)
-constexpr int kLanesK = 32 / kQuads;  // K parts per warp
-constexpr int kThreads = 256;         // compute threads: kKP K parts x kQuads column quads
+constexpr int kCols = 256 / kC;       // output columns per CTA (64): 8 warps x 8
+constexpr int kThreads = 256;         // compute threads (8 warps)
 constexpr int kBlock = kThreads + 32; // + the weight producer warp
-constexpr int kKP = 8 * kLanesK;      // K parts (8 warps)
-constexpr int kRMax = 16;             // rays per cluster tile: 8, 12 or 16, the smallest that fits one round
+constexpr int kR = 16;                // rays per cluster tile (the MMA M dimension)
 constexpr int kHeadK = 1024;          // 16 points x (63 features + 1 zero)
-constexpr int kChunk = 32;            // weights per thread per chunk: 8 K rows x 4 columns
-constexpr int kHeadChunks = kHeadK / kKP / 8;   // 8-row chunks per thread: head (8)
-constexpr int kBodyChunks = 256 / kKP / 8;      // body / tail (2)
+constexpr int kFStride = kHeadK + 4;  // padded rows: the A-fragment loads are bank-conflict free
+constexpr int kXStride = 256 + 4;
+constexpr int kKSteps = 16;           // k-steps of 8 rows per stage (128 K rows)
+constexpr int kHeadStages = kHeadK / (8 * kKSteps);   // 8
+constexpr int kBodyStages = 256 / (8 * kKSteps);      // 2
 constexpr int kLayers = 34;           // head, 32 block layers, fused tail
-constexpr int kStagesPerTile = kHeadChunks + (kLayers - 1) * kBodyChunks;       // 74
-constexpr uint32_t kStageBytes = kThreads * kChunk * 4;                         // 32 KB
+constexpr int kStagesPerTile = kHeadStages + (kLayers - 1) * kBodyStages;       // 74
+constexpr uint32_t kStageBytes = 8 * kKSteps * 32 * 8;                         // 32 KB
 constexpr int kRing = 3;
-constexpr size_t kImageFloats = (size_t)kStagesPerTile * kC * kThreads * kChunk;
+constexpr size_t kImageFloats = (size_t)kStagesPerTile * kC * (kStageBytes / 4);
 
 struct ClSmem {
-  float4 ring[kRing][kStageBytes / 16];   // weight stage slots: float4 i of compute thread t at [256 i + t]
-  float f[kRMax][kHeadK];
-  float x[kRMax][256];
-  float h[kRMax][256];
-  float part[8][kRMax][kCols];   // per warp (its K parts pre-reduced by shuffle)
-  double ray[kRMax][8];
-  uint32_t pix[kRMax], obj[kRMax];
-  int valid[kRMax];
+  float2 ring[kRing][kStageBytes / 8];   // weight stage slots: [warp][k-step][lane] (W[n][k], W[n][k + 4])
+  float f[kR][kFStride];
+  float x[kR][kXStride];
+  float h[kR][kXStride];
+  double ray[kR][8];
+  uint32_t pix[kR], obj[kR];
+  int valid[kR];
   uint64_t full[kRing], empty[kRing];
   uint64_t feat_bar;             // features of the tile: 64 KB from the 4 CTAs
   uint64_t layer_bar[2];         // layer L outputs (16 KB from the 4 CTAs) on layer_bar[L & 1]
 };
+constexpr uint32_t kFeatBytes = kR * kHeadK * 4;
+constexpr uint32_t kLayerBytes = kR * 256 * 4;
 
 // remote store that completes its bytes on the receiving CTA's mbarrier
 __device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uint32_t mbar) {
@@ -80,52 +83,94 @@ __device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uin
                "f"(a), "f"(b), "r"(mbar)
                : "memory");
 }
-__device__ __forceinline__ void st_async_v4(uint32_t addr, float a, float b, float c, float d, uint32_t mbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
-               "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar)
-               : "memory");
-}
 __device__ __forceinline__ void st_async_f32(uint32_t addr, float v, uint32_t mbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(addr), "f"(v),
                "r"(mbar)
                : "memory");
 }
-// acc (two fp32 lanes) += x * (w0, w1), each lane one fma.rn.f32
-__device__ __forceinline__ uint64_t ffma2(float x, uint64_t w, uint64_t acc) {
-  uint64_t d;
-  asm("{\n\t.reg .b64 xx;\n\tmov.b64 xx, {%1, %1};\n\tfma.rn.f32x2 %0, xx, %2, %3;\n\t}"
-      : "=l"(d)
-      : "f"(x), "l"(w), "l"(acc));
-  return d;
+// TF32 split without conversions (cvt.rna.tf32 issues at a quarter rate): hi = x with the 13 low
+// mantissa bits cleared, lo = x - hi (exact in fp32); the MMA reads the top 19 bits of each operand,
+// so lo enters truncated to TF32 -- the split keeps ~2^-21 of |x|.
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = __float_as_uint(x) & 0xFFFFE000u;
+  lo = __float_as_uint(x - __uint_as_float(hi));
 }
-__device__ __forceinline__ uint64_t f2_as_u64(float lo, float hi) {
-  uint64_t d;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
-  return d;
-}
-__device__ __forceinline__ float2 u64_as_f2(uint64_t v) {
-  float2 r;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
-  return r;
+// C[16 x 8] += A[16 x 8] B[8 x 8], TF32 inputs, fp32 accumulation
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 }  // namespace
 
 // optional timeline of cluster 0 / CTA 0 (diagnostics, nedf_diag_cl_trace): per tile i < 4,
-// [64 i + 0] start, [+1] rays set up, [+2] features landed, [+3 + L] layer L landed, [+40] decoded
+// [64 i + 0] start, [+1] rays set up, [+2] features landed, [+3 + L] layer L landed, [+40] decoded,
+// layer 5: [+41] MMAs done (warp 0), [+42] outputs sent
 __device__ unsigned long long g_cl_trace[256];
 __device__ int g_cl_trace_on;
 
-// The compute warps' tile loop for R-ray tiles (R = 8, 12, 16).
-template <int R>
-__device__ __forceinline__ void guard_tiles(ClSmem& S, const int* s_tiles, int total, int ng, const GroupTable& gt,
-                                            const ListSet& ls, const RayJob& job, const OutSpec& out, uint32_t rank,
-                                            int cid, int n_cl) {
+__global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kBlock, 1)
+mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  ClSmem& S = *reinterpret_cast<ClSmem*>(smem_raw);
+  __shared__ int s_tiles[65];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = tc::cluster_rank();
+  const int cid = blockIdx.x / kC, n_cl = gridDim.x / kC;
+  const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
   const bool feats_in = out.feats != nullptr;
+
+  if (tid == 0) {
+    int cum = 0;
+    s_tiles[0] = 0;
+    for (int g = 0; g < ng; ++g) {
+      cum += (ls.count[g] + kR - 1) / kR;
+      s_tiles[g + 1] = cum;
+    }
+    for (int i = 0; i < kRing; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], 8); }
+    tc::mbar_init(&S.feat_bar, 1);
+    tc::mbar_init(&S.layer_bar[0], 1);
+    tc::mbar_init(&S.layer_bar[1], 1);
+    tc::mbar_fence_init();
+  }
+  tc::cluster_sync();           // peers' barriers initialised before anyone stores into them
+  const int total = s_tiles[ng];
+
+  if (warp == 8) {
+    // ---------------------------------------------------------------- weight producer
+    // stage q of a tile = this CTA's 32 KB slice of (head K block q | layer 1 + (q - 8) / 2, K block (q - 8) % 2)
+    // bulk copies issued by one thread serialise, so each stage goes out as kCopyLanes parallel pieces
+    constexpr int kCopyLanes = 4;
+    constexpr uint32_t kPiece = kStageBytes / kCopyLanes;
+    uint32_t gq = 0;
+    for (int t = cid; t < total; t += n_cl) {
+      int g = 0;
+      while (g < ng - 1 && t >= s_tiles[g + 1]) ++g;
+      const unsigned char* img = reinterpret_cast<const unsigned char*>(gt.models[g].wcluster);
+      for (int q = 0; q < kStagesPerTile; ++q, ++gq) {
+        const int slot = gq % kRing;
+        if (lane == 0) {
+          tc::mbar_wait(&S.empty[slot], ((gq / kRing) & 1) ^ 1);
+          tc::mbar_expect_tx(&S.full[slot], kStageBytes);
+        }
+        __syncwarp();
+        if (lane < kCopyLanes)
+          tc::bulk_g2s(reinterpret_cast<unsigned char*>(&S.ring[slot][0]) + lane * kPiece,
+                       img + ((size_t)q * kC + rank) * kStageBytes + lane * kPiece, kPiece, &S.full[slot]);
+      }
+    }
+    __syncwarp();
+    tc::cluster_sync();
+    return;
+  }
+
   // ------------------------------------------------------------------ compute warps
-  const int cg = lane % kQuads, kp = kLanesK * warp + lane / kQuads;
+  const int gid = lane >> 2, tig = lane & 3;          // MMA fragment coordinates
+  const int col = kCols * (int)rank + 8 * warp + 2 * tig;   // this lane's two output columns: col, col + 1
   // shared::cluster address of S in every CTA of the cluster
   uint32_t peer[kC];
 #pragma unroll
@@ -140,11 +185,11 @@ __device__ __forceinline__ void guard_tiles(ClSmem& S, const int* s_tiles, int t
     int g = 0;
     while (g < ng - 1 && t >= s_tiles[g + 1]) ++g;
     const int lt = t - s_tiles[g];
-    int n = ls.count[g] - lt * R;
-    n = n < R ? n : R;
-    const int64_t base = ls.offset[g] + (int64_t)lt * R;
+    int n = ls.count[g] - lt * kR;
+    n = n < kR ? n : kR;
+    const int64_t base = ls.offset[g] + (int64_t)lt * kR;
     const DevModel& m = gt.models[g];
-    if (tid < R) {
+    if (tid < kR) {
       const int r = tid;
       const int v = r < n;
       S.valid[r] = v;
@@ -167,7 +212,7 @@ __device__ __forceinline__ void guard_tiles(ClSmem& S, const int* s_tiles, int t
     // ---- head features: this CTA computes sample points kPtsPerCta rank .. kPtsPerCta (rank + 1) - 1 and broadcasts them
     // (float64, geometry.py:312-342); one (ray, point, coordinate, level) per thread
     constexpr int kPtsPerCta = kPoints / kC;
-    for (int e = tid; e < R * kPtsPerCta * 33; e += kThreads) {
+    for (int e = tid; e < kR * kPtsPerCta * 33; e += kThreads) {
       const int r = e / (kPtsPerCta * 33), rem = e % (kPtsPerCta * 33), p2 = rem / 33, a = (rem / 11) % 3,
                 lev = rem % 11;
       const int pt = kPtsPerCta * (int)rank + p2;
@@ -204,118 +249,95 @@ __device__ __forceinline__ void guard_tiles(ClSmem& S, const int* s_tiles, int t
         }
       }
     }
-    if (tid == 0) tc::mbar_expect_tx(&S.feat_bar, (uint32_t)(R * kHeadK * 4));
+    if (tid == 0) tc::mbar_expect_tx(&S.feat_bar, kFeatBytes);
     tc::mbar_wait(&S.feat_bar, feat_phase);
     feat_phase ^= 1;
     if (tr) g_cl_trace[64 * ti + 2] = clock64();
     // ---- 34 layers: head (K = 1024), 16 x (fc1, fc2), fused tail (nn.py:115-135)
     const float* bias_p = m.bias_pack;
-    constexpr int kOut = kCols / 16;                 // outputs per thread in the reduce phase (4)
-    const int rr = tid >> 4, cc2 = kOut * (tid & 15), col2 = kCols * (int)rank + cc2;   // reduce role
-    float bnext[kOut];
-#pragma unroll
-    for (int u = 0; u < kOut; ++u) bnext[u] = __ldg(bias_p + col2 + u);
+    float2 bnext = *reinterpret_cast<const float2*>(bias_p + col);
     for (int L = 0; L < kLayers; ++L) {
-      const int nch = L == 0 ? kHeadChunks : kBodyChunks;
-      const float* in = L == 0 ? &S.f[0][0] : ((L & 1) ? &S.x[0][0] : &S.h[0][0]);
-      const int ld_in = L == 0 ? kHeadK : 256;
-      float b[kOut];
+      const int nst = L == 0 ? kHeadStages : kBodyStages;
+      const float* A = L == 0 ? &S.f[0][0] : ((L & 1) ? &S.x[0][0] : &S.h[0][0]);
+      const int lda = L == 0 ? kFStride : kXStride;
+      const float2 b = bnext;
+      if (L + 1 < kLayers) bnext = *reinterpret_cast<const float2*>(bias_p + (L + 1) * 256 + col);
+      // twelve independent accumulator chains (lo-hi, hi-lo, hi-hi products x k-step mod 4) so
+      // consecutive MMAs of a warp do not wait on each other's results
+      float acc[12][4];
 #pragma unroll
-      for (int u = 0; u < kOut; ++u) b[u] = bnext[u];
-      if (L + 1 < kLayers) {
-#pragma unroll
-        for (int u = 0; u < kOut; ++u) bnext[u] = __ldg(bias_p + (L + 1) * 256 + col2 + u);
-      }
-      uint64_t acc[R][2];                           // columns (4 cg, 4 cg + 1), (4 cg + 2, 4 cg + 3)
-#pragma unroll
-      for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = 0ull;
-      for (int j = 0; j < nch; ++j) {
-        // this chunk's weights: float4 i = W[c0 .. c0 + 3][k0 + i], copied out of the ring slot, which is
-        // then released to the producer before the FMAs
+      for (int i = 0; i < 12; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+      const float* a_lo_row = A + gid * lda + tig;           // rows gid, gid + 8; columns k0 + tig, k0 + tig + 4
+      const float* a_hi_row = A + (gid + 8) * lda + tig;
+      for (int st = 0; st < nst; ++st) {
+        // this warp's 16 k-steps of the stage, copied out of the ring slot, which is then released
         const int slot = gq % kRing;
+        const long long tw0 = (tr && L == 5) ? clock64() : 0;
         tc::mbar_wait(&S.full[slot], (gq / kRing) & 1);
+        if (tr && L == 5) g_cl_trace[64 * ti + 43] += clock64() - tw0;
         ++gq;
-        uint64_t w[8][2];
+        float2 wv[kKSteps];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float4 v = S.ring[slot][kThreads * i + tid];
-          w[i][0] = f2_as_u64(v.x, v.y);
-          w[i][1] = f2_as_u64(v.z, v.w);
-        }
+        for (int ks = 0; ks < kKSteps; ++ks) wv[ks] = S.ring[slot][(warp * kKSteps + ks) * 32 + lane];
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&S.empty[slot]);
-        const float* inp = in + kp * (8 * nch) + 8 * j;
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const float4 x4 = *reinterpret_cast<const float4*>(inp + r * ld_in + 4 * h2);
-            const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              acc[r][0] = ffma2(xs[e], w[4 * h2 + e][0], acc[r][0]);
-              acc[r][1] = ffma2(xs[e], w[4 * h2 + e][1], acc[r][1]);
-            }
-          }
+        for (int ks = 0; ks < kKSteps; ++ks) {
+          const int k0 = (st * kKSteps + ks) * 8;
+          uint32_t ah[4], al[4], bh0, bl0, bh1, bl1;
+          split_tf32(a_lo_row[k0], ah[0], al[0]);
+          split_tf32(a_hi_row[k0], ah[1], al[1]);
+          split_tf32(a_lo_row[k0 + 4], ah[2], al[2]);
+          split_tf32(a_hi_row[k0 + 4], ah[3], al[3]);
+          split_tf32(wv[ks].x, bh0, bl0);
+          split_tf32(wv[ks].y, bh1, bl1);
+          const int par = 3 * (ks & 3);
+          mma_tf32(acc[par + 0], al, bh0, bh1);
+          mma_tf32(acc[par + 1], ah, bl0, bl1);
+          mma_tf32(acc[par + 2], ah, bh0, bh1);
         }
       }
+      float c[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        c[i] = (((acc[0][i] + acc[3][i]) + (acc[6][i] + acc[9][i])) + ((acc[1][i] + acc[4][i]) + (acc[7][i] + acc[10][i]))) +
+               ((acc[2][i] + acc[5][i]) + (acc[8][i] + acc[11][i]));
       if (tr && L == 5) g_cl_trace[64 * ti + 41] = clock64();
-      if (g_cl_trace_on && cid == 0 && rank == 0 && lane == 0 && ti == 0 && L == 5) g_cl_trace[200 + warp] = clock64();
-      // pre-reduce the warp's K parts (lanes l, l + kQuads, ...), then across the 8 warps
-      float a[R][4];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const float2 lo = u64_as_f2(acc[r][0]), hi = u64_as_f2(acc[r][1]);
-        a[r][0] = lo.x; a[r][1] = lo.y; a[r][2] = hi.x; a[r][3] = hi.y;
+      // epilogue: rows gid / gid + 8, columns col / col + 1 (c0 c1 / c2 c3)
+      float v[4];
+      float* dst0;
+      float* dst1;
+      if (L == 0 || L == kLayers - 1) {                         // head (no activation) / tail logits
+        v[0] = c[0] + b.x; v[1] = c[1] + b.y; v[2] = c[2] + b.x; v[3] = c[3] + b.y;
+        float* base_buf = L == 0 ? &S.x[0][0] : &S.h[0][0];
+        dst0 = base_buf + gid * kXStride + col;
+        dst1 = base_buf + (gid + 8) * kXStride + col;
+      } else if (L & 1) {                                       // fc1
+        v[0] = fmaxf(c[0] + b.x, 0.f); v[1] = fmaxf(c[1] + b.y, 0.f);
+        v[2] = fmaxf(c[2] + b.x, 0.f); v[3] = fmaxf(c[3] + b.y, 0.f);
+        dst0 = &S.h[gid][col];
+        dst1 = &S.h[gid + 8][col];
+      } else {                                                  // fc2 + residual
+        dst0 = &S.x[gid][col];
+        dst1 = &S.x[gid + 8][col];
+        v[0] = dst0[0] + fmaxf(c[0] + b.x, 0.f); v[1] = dst0[1] + fmaxf(c[1] + b.y, 0.f);
+        v[2] = dst1[0] + fmaxf(c[2] + b.x, 0.f); v[3] = dst1[1] + fmaxf(c[3] + b.y, 0.f);
       }
+      const int lb = layer_count & 1;
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int off = kQuads; off < 32; off <<= 1) a[r][u] += __shfl_xor_sync(0xffffffffu, a[r][u], off);
-      if (lane < kQuads) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          *reinterpret_cast<float4*>(&S.part[warp][r][4 * cg]) = make_float4(a[r][0], a[r][1], a[r][2], a[r][3]);
+      for (int qq = 0; qq < kC; ++qq) {
+        const uint32_t bar = remote(qq, &S.layer_bar[lb]);
+        st_async_v2(remote(qq, dst0), v[0], v[1], bar);
+        st_async_v2(remote(qq, dst1), v[2], v[3], bar);
       }
-      tc::named_bar(1, kThreads);
       if (tr && L == 5) g_cl_trace[64 * ti + 42] = clock64();
-      if (rr < R) {   // kOut adjacent outputs per thread: R rays x kCols columns
-        float sv[kOut];
-#pragma unroll
-        for (int u = 0; u < kOut; ++u) sv[u] = 0.f;
-#pragma unroll
-        for (int w8 = 0; w8 < 8; ++w8)
-#pragma unroll
-          for (int u = 0; u < kOut; ++u) sv[u] += S.part[w8][rr][cc2 + u];
-        float v[kOut];
-        float* dst;
-        if (L == 0 || L == kLayers - 1) {                         // head (no activation) / tail logits
-#pragma unroll
-          for (int u = 0; u < kOut; ++u) v[u] = sv[u] + b[u];
-          dst = L == 0 ? &S.x[rr][col2] : &S.h[rr][col2];
-        } else if (L & 1) {                                       // fc1
-#pragma unroll
-          for (int u = 0; u < kOut; ++u) v[u] = fmaxf(sv[u] + b[u], 0.f);
-          dst = &S.h[rr][col2];
-        } else {                                                  // fc2 + residual
-#pragma unroll
-          for (int u = 0; u < kOut; ++u) v[u] = S.x[rr][col2 + u] + fmaxf(sv[u] + b[u], 0.f);
-          dst = &S.x[rr][col2];
-        }
-        const int lb = layer_count & 1;
-#pragma unroll
-        for (int qq = 0; qq < kC; ++qq) st_async_v4(remote(qq, dst), v[0], v[1], v[2], v[3], remote(qq, &S.layer_bar[lb]));
-      }
-      if (tr && L == 5) g_cl_trace[64 * ti + 43] = clock64();
-      if (tid == 0) tc::mbar_expect_tx(&S.layer_bar[layer_count & 1], (uint32_t)(R * 256 * 4));
-      tc::mbar_wait(&S.layer_bar[layer_count & 1], (layer_count >> 1) & 1);
+      if (tid == 0) tc::mbar_expect_tx(&S.layer_bar[lb], kLayerBytes);
+      tc::mbar_wait(&S.layer_bar[lb], (layer_count >> 1) & 1);
       ++layer_count;
       if (tr) g_cl_trace[64 * ti + 3 + L] = clock64();
     }
     // ---- decode: fine = logits[0:128), coarse = [128:192), alpha = [192] (model.py:277-293)
-    if (rank == 0 && tid < R && S.valid[tid]) {
+    if (rank == 0 && tid < kR && S.valid[tid]) {
       const int r = tid;
       const float* lg = S.h[r];
       if (out.mode == OUT_LOGITS) {
@@ -337,71 +359,6 @@ __device__ __forceinline__ void guard_tiles(ClSmem& S, const int* s_tiles, int t
     tc::named_bar(1, kThreads);
     if (tr) g_cl_trace[64 * ti + 40] = clock64();
   }
-}
-
-__global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kBlock, 1)
-mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  ClSmem& S = *reinterpret_cast<ClSmem*>(smem_raw);
-  __shared__ int s_tiles[65];
-  __shared__ int s_R;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const uint32_t rank = tc::cluster_rank();
-  const int cid = blockIdx.x / kC, n_cl = gridDim.x / kC;
-  const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
-
-  if (tid == 0) {
-    // tile size: the smallest of 8, 12, 16 rays whose tiles all run in one round of clusters (the
-    // per-layer FMA time scales with the rays per tile, the exchange latency does not)
-    int R = 16;
-    for (int cand = 8; cand < 16; cand += 4) {
-      int tiles = 0;
-      for (int g = 0; g < ng; ++g) tiles += (ls.count[g] + cand - 1) / cand;
-      if (tiles <= n_cl) { R = cand; break; }
-    }
-    s_R = R;
-    int cum = 0;
-    s_tiles[0] = 0;
-    for (int g = 0; g < ng; ++g) {
-      cum += (ls.count[g] + R - 1) / R;
-      s_tiles[g + 1] = cum;
-    }
-    for (int i = 0; i < kRing; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], 8); }
-    tc::mbar_init(&S.feat_bar, 1);
-    tc::mbar_init(&S.layer_bar[0], 1);
-    tc::mbar_init(&S.layer_bar[1], 1);
-    tc::mbar_fence_init();
-  }
-  tc::cluster_sync();           // peers' barriers initialised before anyone stores into them
-  const int total = s_tiles[ng];
-
-  if (warp == 8) {
-    // ---------------------------------------------------------------- weight producer
-    // stage q of a tile = this CTA's 32 KB slice of (head chunk q | layer 1 + (q - 8) / 2, chunk (q - 8) % 2)
-    if (lane == 0) {
-      uint32_t gq = 0;
-      for (int t = cid; t < total; t += n_cl) {
-        int g = 0;
-        while (g < ng - 1 && t >= s_tiles[g + 1]) ++g;
-        const unsigned char* img = reinterpret_cast<const unsigned char*>(gt.models[g].wcluster);
-        for (int q = 0; q < kStagesPerTile; ++q, ++gq) {
-          const int slot = gq % kRing;
-          tc::mbar_wait(&S.empty[slot], ((gq / kRing) & 1) ^ 1);
-          tc::mbar_expect_tx(&S.full[slot], kStageBytes);
-          tc::bulk_g2s(&S.ring[slot][0], img + ((size_t)q * kC + rank) * kStageBytes, kStageBytes, &S.full[slot]);
-        }
-      }
-    }
-    __syncwarp();
-    tc::cluster_sync();
-    return;
-  }
-
-  // ------------------------------------------------------------------ compute warps
-  if (s_R == 8) guard_tiles<8>(S, s_tiles, total, ng, gt, ls, job, out, rank, cid, n_cl);
-  else if (s_R == 12) guard_tiles<12>(S, s_tiles, total, ng, gt, ls, job, out, rank, cid, n_cl);
-  else guard_tiles<16>(S, s_tiles, total, ng, gt, ls, job, out, rank, cid, n_cl);
   tc::cluster_sync();           // no CTA leaves while its stores to peers may be in flight
 }
 
@@ -444,13 +401,13 @@ cudaError_t launch_mlp_fp32_cluster(const GroupTable& gt, const ListSet& ls, con
   return cudaGetLastError();
 }
 
-// Cluster image, streamed as 32 KB stages: stage q (head chunk q < 8, then layer
-// L = 1 + (q - 8) / 2, chunk j = (q - 8) % 2), CTA r -> float4 [(q kC + r) 2048 +
-// 256 i + t] = W[c0 .. c0 + 3][k] for compute thread t (column quad cg = t & 15,
-// K part kp = 2 (t >> 5) + ((t >> 4) & 1)), K row k = kp * 8 n + 8 j + i (n =
-// chunks of the layer: 8 for the head, 2 after) and c0 = 64 r + 4 cg (head rows
-// are the 16 points' 63 features + 1 zero; tail outputs: fine 0-127, coarse
-// 128-191, alpha 192).  Thread-minor float4s make each ring read conflict-free.
+// Cluster image, streamed as 32 KB stages: stage q (head K block q < 8, then
+// layer L = 1 + (q - 8) / 2, K block j = (q - 8) % 2), CTA r -> float2
+// [(q kC + r) 4096 + (16 w + s) 32 + lane] = (W[n][k], W[n][k + 4]) for warp w,
+// k-step s, lane = 4 gid + tig: output column n = 64 r + 8 w + gid, K row
+// k = 128 j + 8 s + tig (the B fragment of an m16n8k8 MMA).  Head rows are the
+// 16 points' 63 features + 1 zero; tail outputs: fine 0-127, coarse 128-191,
+// alpha 192, zero padding.
 cudaError_t fp32_pack_cluster(const float* P, int d_in, int F, int n_blocks, int n_coarse, int n_fine, float** dev) {
   if (F != 256 || n_blocks != 16 || d_in != kDin || n_coarse != 64 || n_fine != 128) return cudaErrorInvalidValue;
   std::vector<float> img(kImageFloats, 0.f);
@@ -471,19 +428,18 @@ cudaError_t fp32_pack_cluster(const float* P, int d_in, int F, int n_blocks, int
     return 0.f;
   };
   for (int q = 0; q < kStagesPerTile; ++q) {
-    const int L = q < kHeadChunks ? 0 : 1 + (q - kHeadChunks) / kBodyChunks;
-    const int j = q < kHeadChunks ? q : (q - kHeadChunks) % kBodyChunks;
-    const int nch = L == 0 ? kHeadChunks : kBodyChunks;
+    const int L = q < kHeadStages ? 0 : 1 + (q - kHeadStages) / kBodyStages;
+    const int j = q < kHeadStages ? q : (q - kHeadStages) % kBodyStages;
     for (int r = 0; r < kC; ++r)
-      for (int t = 0; t < kThreads; ++t) {
-        const int lane = t & 31, cg = lane % kQuads, kp = kLanesK * (t >> 5) + lane / kQuads;
-        const int c0 = kCols * r + 4 * cg;
-        for (int i = 0; i < 8; ++i) {
-          float* dst = img.data() + 4 * (((size_t)q * kC + r) * (kStageBytes / 16) + (size_t)kThreads * i + t);
-          const int k = kp * 8 * nch + 8 * j + i;
-          for (int u = 0; u < 4; ++u) dst[u] = w_of(L, c0 + u, k);
-        }
-      }
+      for (int w = 0; w < 8; ++w)
+        for (int s = 0; s < kKSteps; ++s)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int n = kCols * r + 8 * w + (lane >> 2);
+            const int k = 8 * kKSteps * j + 8 * s + (lane & 3);
+            float* dst = img.data() + 2 * (((size_t)q * kC + r) * (kStageBytes / 8) + (size_t)(w * kKSteps + s) * 32 + lane);
+            dst[0] = w_of(L, n, k);
+            dst[1] = w_of(L, n, k + 4);
+          }
   }
   cudaError_t e = cudaMalloc(dev, img.size() * sizeof(float));
   if (e == cudaSuccess) e = cudaMemcpy(*dev, img.data(), img.size() * sizeof(float), cudaMemcpyHostToDevice);

@@ -34,6 +34,6 @@ for i in range(4):
           f"L33 {layers[33]} decoded {rel(40)}")
     d = [layers[L + 1] - layers[L] for L in range(33) if layers[L + 1] and layers[L]]
     print("   per-layer cycles:", d[:8], "...", d[-4:])
-    print("   layer 5: fma", t[64 * i + 41] - t[64 * i + 3 + 4], "reduce-sync", t[64 * i + 42] - t[64 * i + 41],
-          "reduce+stores", t[64 * i + 43] - t[64 * i + 42], "wait", t[64 * i + 3 + 5] - t[64 * i + 43])
+    print("   layer 5: MMAs", t[64 * i + 41] - t[64 * i + 3 + 4], "(of which weight-ring waits", t[64 * i + 43], ")",
+          "epilogue + sends", t[64 * i + 42] - t[64 * i + 41], "wait for peers", t[64 * i + 3 + 5] - t[64 * i + 42])
 print("layer 5 FMA end per warp (tile 0, rel. to layer start):", [t[200 + w] - t[3 + 4] if t[200 + w] else None for w in range(16)])
