@@ -71,21 +71,14 @@ struct ClSmem {
   uint32_t pix[kR], obj[kR];
   int valid[kR];
   uint64_t full[kRing], empty[kRing];
-  uint64_t feat_bar;             // features of the tile: 64 KB from the 4 CTAs
   uint64_t layer_bar[2];         // layer L outputs (16 KB from the 4 CTAs) on layer_bar[L & 1]
 };
-constexpr uint32_t kFeatBytes = kR * kHeadK * 4;
 constexpr uint32_t kLayerBytes = kR * 256 * 4;
 
 // remote store that completes its bytes on the receiving CTA's mbarrier
 __device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uint32_t mbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr),
                "f"(a), "f"(b), "r"(mbar)
-               : "memory");
-}
-__device__ __forceinline__ void st_async_f32(uint32_t addr, float v, uint32_t mbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(addr), "f"(v),
-               "r"(mbar)
                : "memory");
 }
 // TF32 split without conversions (cvt.rna.tf32 issues at a quarter rate): hi = x with the 13 low
@@ -132,7 +125,6 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       s_tiles[g + 1] = cum;
     }
     for (int i = 0; i < kRing; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], 8); }
-    tc::mbar_init(&S.feat_bar, 1);
     tc::mbar_init(&S.layer_bar[0], 1);
     tc::mbar_init(&S.layer_bar[1], 1);
     tc::mbar_fence_init();
@@ -177,7 +169,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
   for (int q = 0; q < kC; ++q) peer[q] = tc::peer_addr(&S, q);
   const uint32_t self = tc::smem_u32(&S);
   auto remote = [&](int q, const void* p) { return peer[q] + (uint32_t)(tc::smem_u32(p) - self); };
-  uint32_t feat_phase = 0, layer_count = 0, gq = 0;
+  uint32_t layer_count = 0, gq = 0;
   int ti = 0;
   for (int t = cid; t < total; t += n_cl, ++ti) {
     const bool tr = g_cl_trace_on && cid == 0 && rank == 0 && tid == 0 && ti < 4;
@@ -209,49 +201,43 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
     }
     tc::named_bar(1, kThreads);
     if (tr) g_cl_trace[64 * ti + 1] = clock64();
-    // ---- head features: this CTA computes sample points kPtsPerCta rank .. kPtsPerCta (rank + 1) - 1 and broadcasts them
-    // (float64, geometry.py:312-342); one (ray, point, coordinate, level) per thread
-    constexpr int kPtsPerCta = kPoints / kC;
-    for (int e = tid; e < kR * kPtsPerCta * 33; e += kThreads) {
-      const int r = e / (kPtsPerCta * 33), rem = e % (kPtsPerCta * 33), p2 = rem / 33, a = (rem / 11) % 3,
-                lev = rem % 11;
-      const int pt = kPtsPerCta * (int)rank + p2;
-      float v0 = 0.f, v1 = 0.f;       // lev < 10: sin, cos; lev 10: raw p, pad
-      if (S.valid[r]) {
-        if (feats_in) {
-          const float* src = out.feats + (size_t)S.pix[r] * kDin + pt * kPerPoint + 21 * a;
-          if (lev < 10) { v0 = src[1 + 2 * lev]; v1 = src[2 + 2 * lev]; }
-          else v0 = src[0];
-        } else {
-          const double t0 = S.ray[r][6], t1 = S.ray[r][7];
-          const double tt = t0 + (t1 - t0) * lin16(pt);
-          const double p = ((S.ray[r][a] + tt * S.ray[r][3 + a]) - m.c[a]) / m.h[a];
-          if (lev < 10) {
-            double sn, cs;
-            sincospi(ldexp(p, lev), &sn, &cs);     // sin/cos(2^lev pi p), exact argument scaling
-            v0 = (float)sn;
-            v1 = (float)cs;
-          } else {
-            v0 = (float)p;
+    // ---- head features (float64, geometry.py:312-342), computed by every CTA of the cluster for itself:
+    // one (ray, point, coordinate) per thread, sin/cos at levels 0 and 5 with exact argument scaling,
+    // the other levels by float64 double-angle steps (error ~1e-15, far below the float32 rounding)
+    for (int e = tid; e < kR * kPoints * 3; e += kThreads) {
+      const int r = e / (kPoints * 3), rem = e % (kPoints * 3), pt = rem / 3, a = rem % 3;
+      float* dst = &S.f[r][64 * pt + 21 * a];
+      if (!S.valid[r]) {
+#pragma unroll
+        for (int j = 0; j < 21; ++j) dst[j] = 0.f;
+      } else if (feats_in) {
+        const float* src = out.feats + (size_t)S.pix[r] * kDin + pt * kPerPoint + 21 * a;
+#pragma unroll
+        for (int j = 0; j < 21; ++j) dst[j] = src[j];
+      } else {
+        const double t0 = S.ray[r][6], t1 = S.ray[r][7];
+        const double tt = t0 + (t1 - t0) * lin16(pt);
+        const double p = ((S.ray[r][a] + tt * S.ray[r][3 + a]) - m.c[a]) / m.h[a];
+        dst[0] = (float)p;
+#pragma unroll
+        for (int base = 0; base < kLevels; base += 5) {
+          double sn, cs;
+          sincospi(ldexp(p, base), &sn, &cs);
+          dst[1 + 2 * base] = (float)sn;
+          dst[2 + 2 * base] = (float)cs;
+#pragma unroll
+          for (int k = base + 1; k < base + 5; ++k) {
+            const double s2 = 2.0 * sn * cs, c2 = (cs - sn) * (cs + sn);
+            sn = s2;
+            cs = c2;
+            dst[1 + 2 * k] = (float)sn;
+            dst[2 + 2 * k] = (float)cs;
           }
         }
       }
-      float* dst = &S.f[r][64 * pt + 21 * a];
-#pragma unroll
-      for (int q = 0; q < kC; ++q) {
-        const uint32_t fb = remote(q, &S.feat_bar);
-        if (lev < 10) {
-          st_async_f32(remote(q, dst + 1 + 2 * lev), v0, fb);     // odd offsets for a = 0: no v2
-          st_async_f32(remote(q, dst + 2 + 2 * lev), v1, fb);
-        } else {
-          st_async_f32(remote(q, dst), v0, fb);
-          if (a == 0) st_async_f32(remote(q, &S.f[r][64 * pt + 63]), 0.f, fb);
-        }
-      }
+      if (a == 0) S.f[r][64 * pt + 63] = 0.f;
     }
-    if (tid == 0) tc::mbar_expect_tx(&S.feat_bar, kFeatBytes);
-    tc::mbar_wait(&S.feat_bar, feat_phase);
-    feat_phase ^= 1;
+    tc::named_bar(1, kThreads);
     if (tr) g_cl_trace[64 * ti + 2] = clock64();
     // ---- 34 layers: head (K = 1024), 16 x (fc1, fc2), fused tail (nn.py:115-135)
     const float* bias_p = m.bias_pack;
