@@ -71,14 +71,14 @@ struct ClSmem {
   uint32_t pix[kR], obj[kR];
   int valid[kR];
   uint64_t full[kRing], empty[kRing];
-  uint64_t layer_bar[2];         // layer L outputs (16 KB from the 4 CTAs) on layer_bar[L & 1]
+  uint64_t layer_bar[2];         // layer L outputs on layer_bar[L & 1]: 12 KB from the 3 peers + the 8 local warps' arrivals
 };
-constexpr uint32_t kLayerBytes = kR * 256 * 4;
+constexpr uint32_t kPeerBytes = (kC - 1) * kR * kCols * 4;   // 12 KB: the peers' columns of one layer
 
 // remote store that completes its bytes on the receiving CTA's mbarrier
-__device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uint32_t mbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr),
-               "f"(a), "f"(b), "r"(mbar)
+__device__ __forceinline__ void st_async_v4(uint32_t addr, float a, float b, float c, float d, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+               "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar)
                : "memory");
 }
 // TF32 split without conversions (cvt.rna.tf32 issues at a quarter rate): hi = x with the 13 low
@@ -125,8 +125,8 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       s_tiles[g + 1] = cum;
     }
     for (int i = 0; i < kRing; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], 8); }
-    tc::mbar_init(&S.layer_bar[0], 1);
-    tc::mbar_init(&S.layer_bar[1], 1);
+    tc::mbar_init(&S.layer_bar[0], 1 + 8);     // tid 0's expect_tx + one arrival per compute warp
+    tc::mbar_init(&S.layer_bar[1], 1 + 8);
     tc::mbar_fence_init();
   }
   tc::cluster_sync();           // peers' barriers initialised before anyone stores into them
@@ -309,15 +309,24 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
         v[0] = dst0[0] + fmaxf(c[0] + b.x, 0.f); v[1] = dst0[1] + fmaxf(c[1] + b.y, 0.f);
         v[2] = dst1[0] + fmaxf(c[2] + b.x, 0.f); v[3] = dst1[1] + fmaxf(c[3] + b.y, 0.f);
       }
+      // lanes t, t ^ 1 of a quad swap halves so each sends one 16-byte run: the even lane row gid,
+      // columns col .. col + 3; the odd lane row gid + 8, columns col - 2 .. col + 1 (half the remote stores)
+      const bool odd = tig & 1;
+      const float r0 = __shfl_xor_sync(0xffffffffu, odd ? v[0] : v[2], 1);
+      const float r1 = __shfl_xor_sync(0xffffffffu, odd ? v[1] : v[3], 1);
+      float* dst = odd ? dst1 - 2 : dst0;
+      const float4 o4 = odd ? make_float4(r0, r1, v[2], v[3]) : make_float4(v[0], v[1], r0, r1);
       const int lb = layer_count & 1;
 #pragma unroll
-      for (int qq = 0; qq < kC; ++qq) {
-        const uint32_t bar = remote(qq, &S.layer_bar[lb]);
-        st_async_v2(remote(qq, dst0), v[0], v[1], bar);
-        st_async_v2(remote(qq, dst1), v[2], v[3], bar);
+      for (int qq = 1; qq < kC; ++qq) {       // the peers, through distributed shared memory
+        const int peer_rank = ((int)rank + qq) % kC;
+        st_async_v4(remote(peer_rank, dst), o4.x, o4.y, o4.z, o4.w, remote(peer_rank, &S.layer_bar[lb]));
       }
+      *reinterpret_cast<float4*>(dst) = o4;     // this CTA: a plain store, published by the warp's arrival
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&S.layer_bar[lb]);
       if (tr && L == 5) g_cl_trace[64 * ti + 42] = clock64();
-      if (tid == 0) tc::mbar_expect_tx(&S.layer_bar[lb], kLayerBytes);
+      if (tid == 0) tc::mbar_expect_tx(&S.layer_bar[lb], kPeerBytes);
       tc::mbar_wait(&S.layer_bar[lb], (layer_count >> 1) & 1);
       ++layer_count;
       if (tr) g_cl_trace[64 * ti + 3 + L] = clock64();
