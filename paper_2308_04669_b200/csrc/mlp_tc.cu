@@ -157,7 +157,12 @@ __device__ __forceinline__ void encode_point_tc(const double p[3], float f[64]) 
 
 }  // namespace
 
-// optional timeline of CTA 0's second tile (diagnostics, nedf_diag_tc_trace)
+// optional timeline of CTA 0's second tile (diagnostics, nedf_diag_tc_trace).  Compiled in only with
+// -DNEDF_TC_TRACE=1 (scripts/build_variant.py): the instrumentation's registers push the epilogue's
+// residual stream into local memory.
+#ifndef NEDF_TC_TRACE
+#define NEDF_TC_TRACE 0
+#endif
 __device__ unsigned long long g_tc_trace[1024];
 __device__ int g_tc_trace_on;
 __device__ __forceinline__ void trace_at(bool on, int idx) {
@@ -174,6 +179,45 @@ __device__ __forceinline__ void twait(uint64_t* bar, uint32_t ph, bool on, unsig
     acc += clock64() - t0;
   } else {
     if (NEDF_TC_SPIN) tc::mbar_spin(bar, ph); else tc::mbar_wait(bar, ph);
+  }
+}
+
+// One epilogue slice half: this thread's 64 accumulator columns [col0, col0 + 64) as four
+// 16-column chunks, the TMEM load of chunk c + 1 in flight while chunk c is processed (16
+// registers per buffer keeps the residual stream x in registers).  MODE 0: head, x = acc + b;
+// 1: fc1, h = relu(acc + b) -> fp16 into A_Q; 2: fc2, x += relu(acc + b) -> fp16(x) into A_P.
+template <int MODE>
+__device__ __forceinline__ void epi_half(uint32_t acc_addr, uint32_t dst_addr, const float* bias, float (&xs)[2][32]) {
+  uint32_t va[16], vb[16];
+  tc::tmem_ld16(acc_addr, va);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    tc::tmem_ld_wait();
+    uint32_t (&v)[16] = (c & 1) ? vb : va;
+    if (c < 3) tc::tmem_ld16(acc_addr + 16 * (c + 1), (c & 1) ? va : vb);
+    float* xc = &xs[c >> 1][16 * (c & 1)];
+    const float4* b4 = reinterpret_cast<const float4*>(bias + 16 * c);
+    uint32_t pk[8];
+#pragma unroll
+    for (int j4 = 0; j4 < 4; ++j4) {
+      const float4 b = b4[j4];
+      const float a0 = __uint_as_float(v[4 * j4 + 0]) + b.x, a1 = __uint_as_float(v[4 * j4 + 1]) + b.y;
+      const float a2 = __uint_as_float(v[4 * j4 + 2]) + b.z, a3 = __uint_as_float(v[4 * j4 + 3]) + b.w;
+      if (MODE == 1) {
+        pk[2 * j4 + 0] = tc::pack_h2_relu(a0, a1);
+        pk[2 * j4 + 1] = tc::pack_h2_relu(a2, a3);
+      } else {
+        if (MODE == 0) {
+          xc[4 * j4 + 0] = a0; xc[4 * j4 + 1] = a1; xc[4 * j4 + 2] = a2; xc[4 * j4 + 3] = a3;
+        } else {
+          xc[4 * j4 + 0] += fmaxf(a0, 0.f); xc[4 * j4 + 1] += fmaxf(a1, 0.f);
+          xc[4 * j4 + 2] += fmaxf(a2, 0.f); xc[4 * j4 + 3] += fmaxf(a3, 0.f);
+        }
+        pk[2 * j4 + 0] = tc::pack_h2(xc[4 * j4 + 0], xc[4 * j4 + 1]);
+        pk[2 * j4 + 1] = tc::pack_h2(xc[4 * j4 + 2], xc[4 * j4 + 3]);
+      }
+    }
+    tc::tmem_st8(dst_addr + 8 * c, pk);
   }
 }
 
@@ -196,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
   const int lane = tid & 31;
   const ListSet& ls = a.ls;
   const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
-  const bool trace_cta = g_tc_trace_on && blockIdx.x == 0;
+  const bool trace_cta = NEDF_TC_TRACE && g_tc_trace_on && blockIdx.x == 0;
   const int trace_tile = g_tc_trace_on;   // nedf_diag_tc_trace(k): timeline of tile k
   const uint32_t rank = csize > 1 ? tc::cluster_rank() : 0;
   const int cid = blockIdx.x / csize, n_cl = gridDim.x / csize;
@@ -453,25 +497,9 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
         tc::mbar_wait(&S.acc_full[s], layer_ctr & 1);
         tc::tc_fence_after();
         trace_at(tr, 100 + s);
-#pragma unroll
-        for (int j2 = 0; j2 < 2; ++j2) {
-          const int col = 128 * s + 64 * hc + 32 * j2;
-          const float4* b4 = reinterpret_cast<const float4*>(bias_s + col);
-          uint32_t v[32];
-          tc::tmem_ld32(lane_addr + kAccCol + col, v);
-          tc::tmem_ld_wait();
-          uint32_t pk[16];
-#pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 b = b4[j4];
-            x[s][j2][4 * j4 + 0] = __uint_as_float(v[4 * j4 + 0]) + b.x;
-            x[s][j2][4 * j4 + 1] = __uint_as_float(v[4 * j4 + 1]) + b.y;
-            x[s][j2][4 * j4 + 2] = __uint_as_float(v[4 * j4 + 2]) + b.z;
-            x[s][j2][4 * j4 + 3] = __uint_as_float(v[4 * j4 + 3]) + b.w;
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) pk[j] = tc::pack_h2(x[s][j2][2 * j], x[s][j2][2 * j + 1]);
-          tc::tmem_st16(lane_addr + kAPCol + col / 2, pk);
+        {
+          const int col = 128 * s + 64 * hc;
+          epi_half<0>(lane_addr + kAccCol + col, lane_addr + kAPCol + col / 2, bias_s + col, x[s]);
         }
         tc::tmem_st_wait();
         tc::tc_fence_before();
@@ -490,23 +518,9 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           tc::mbar_wait(&S.acc_full[s], layer_ctr & 1);
           tc::tc_fence_after();
           trace_at(tr, 100 + l1 * 8 + s);
-#pragma unroll
-          for (int j2 = 0; j2 < 2; ++j2) {
-            const int col = 128 * s + 64 * hc + 32 * j2;
-            const float4* b4 = reinterpret_cast<const float4*>(b1 + col);
-            uint32_t v[32];
-            tc::tmem_ld32(lane_addr + kAccCol + col, v);
-            tc::tmem_ld_wait();
-            uint32_t pk[16];
-#pragma unroll
-            for (int j4 = 0; j4 < 8; ++j4) {
-              const float4 b = b4[j4];
-              pk[2 * j4 + 0] =
-                  tc::pack_h2_relu(__uint_as_float(v[4 * j4 + 0]) + b.x, __uint_as_float(v[4 * j4 + 1]) + b.y);
-              pk[2 * j4 + 1] =
-                  tc::pack_h2_relu(__uint_as_float(v[4 * j4 + 2]) + b.z, __uint_as_float(v[4 * j4 + 3]) + b.w);
-            }
-            tc::tmem_st16(lane_addr + kAQCol + col / 2, pk);
+          {
+            const int col = 128 * s + 64 * hc;
+            epi_half<1>(lane_addr + kAccCol + col, lane_addr + kAQCol + col / 2, b1 + col, x[s]);
           }
           tc::tmem_st_wait();
           tc::tc_fence_before();
@@ -520,25 +534,9 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           tc::mbar_wait(&S.acc_full[s], layer_ctr & 1);
           tc::tc_fence_after();
           trace_at(tr, 100 + (l1 + 1) * 8 + s);
-#pragma unroll
-          for (int j2 = 0; j2 < 2; ++j2) {
-            const int col = 128 * s + 64 * hc + 32 * j2;
-            const float4* b4 = reinterpret_cast<const float4*>(b2 + col);
-            uint32_t v[32];
-            tc::tmem_ld32(lane_addr + kAccCol + col, v);
-            tc::tmem_ld_wait();
-            uint32_t pk[16];
-#pragma unroll
-            for (int j4 = 0; j4 < 8; ++j4) {
-              const float4 b = b4[j4];
-              x[s][j2][4 * j4 + 0] += fmaxf(__uint_as_float(v[4 * j4 + 0]) + b.x, 0.f);
-              x[s][j2][4 * j4 + 1] += fmaxf(__uint_as_float(v[4 * j4 + 1]) + b.y, 0.f);
-              x[s][j2][4 * j4 + 2] += fmaxf(__uint_as_float(v[4 * j4 + 2]) + b.z, 0.f);
-              x[s][j2][4 * j4 + 3] += fmaxf(__uint_as_float(v[4 * j4 + 3]) + b.w, 0.f);
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) pk[j] = tc::pack_h2(x[s][j2][2 * j], x[s][j2][2 * j + 1]);
-            tc::tmem_st16(lane_addr + kAPCol + col / 2, pk);
+          {
+            const int col = 128 * s + 64 * hc;
+            epi_half<2>(lane_addr + kAccCol + col, lane_addr + kAPCol + col / 2, b2 + col, x[s]);
           }
           tc::tmem_st_wait();
           tc::tc_fence_before();
