@@ -111,6 +111,11 @@ __device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
 __device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
+__device__ __forceinline__ float2 f2unpack2(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
 __device__ __forceinline__ uint64_t add_f2(uint64_t a, uint64_t b) {
   uint64_t d;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -201,8 +206,11 @@ __device__ __forceinline__ void epi_half(uint32_t acc_addr, uint32_t dst_addr, c
 #pragma unroll
     for (int j4 = 0; j4 < 4; ++j4) {
       const float4 b = b4[j4];
-      const float a0 = __uint_as_float(v[4 * j4 + 0]) + b.x, a1 = __uint_as_float(v[4 * j4 + 1]) + b.y;
-      const float a2 = __uint_as_float(v[4 * j4 + 2]) + b.z, a3 = __uint_as_float(v[4 * j4 + 3]) + b.w;
+      const float2 a01 = f2unpack2(add_f2(f2pack(__uint_as_float(v[4 * j4 + 0]), __uint_as_float(v[4 * j4 + 1])),
+                                          f2pack(b.x, b.y)));
+      const float2 a23 = f2unpack2(add_f2(f2pack(__uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3])),
+                                          f2pack(b.z, b.w)));
+      const float a0 = a01.x, a1 = a01.y, a2 = a23.x, a3 = a23.y;
       if (MODE == 1) {
         pk[2 * j4 + 0] = tc::pack_h2_relu(a0, a1);
         pk[2 * j4 + 1] = tc::pack_h2_relu(a2, a3);
@@ -210,8 +218,10 @@ __device__ __forceinline__ void epi_half(uint32_t acc_addr, uint32_t dst_addr, c
         if (MODE == 0) {
           xc[4 * j4 + 0] = a0; xc[4 * j4 + 1] = a1; xc[4 * j4 + 2] = a2; xc[4 * j4 + 3] = a3;
         } else {
-          xc[4 * j4 + 0] += fmaxf(a0, 0.f); xc[4 * j4 + 1] += fmaxf(a1, 0.f);
-          xc[4 * j4 + 2] += fmaxf(a2, 0.f); xc[4 * j4 + 3] += fmaxf(a3, 0.f);
+          // x += relu(acc + b) as f32x2 adds (same rn operations, half the issue slots)
+          float2 x01 = f2unpack2(add_f2(f2pack(xc[4 * j4 + 0], xc[4 * j4 + 1]), f2pack(fmaxf(a0, 0.f), fmaxf(a1, 0.f))));
+          float2 x23 = f2unpack2(add_f2(f2pack(xc[4 * j4 + 2], xc[4 * j4 + 3]), f2pack(fmaxf(a2, 0.f), fmaxf(a3, 0.f))));
+          xc[4 * j4 + 0] = x01.x; xc[4 * j4 + 1] = x01.y; xc[4 * j4 + 2] = x23.x; xc[4 * j4 + 3] = x23.y;
         }
         pk[2 * j4 + 0] = tc::pack_h2(xc[4 * j4 + 0], xc[4 * j4 + 1]);
         pk[2 * j4 + 1] = tc::pack_h2(xc[4 * j4 + 2], xc[4 * j4 + 3]);

@@ -1,6 +1,11 @@
 #!/usr/bin/env python3
 """Print the per-role timeline of one steady-state tile of the tcgen05 kernel
-(CTA 0, its second tile) while rendering STEP 1 of the config-4 frame."""
+(CTA 0, its second tile) while rendering STEP 1 of the config-4 frame.
+
+The instrumentation is compiled in only with -DNEDF_TC_TRACE=1:
+    python scripts/build_variant.py trace mlp_tc.cu -DNEDF_TC_TRACE=1
+    NEDF_LIB=_exp/trace.so python scripts/tc_trace.py 3 3
+"""
 
 import ctypes as C
 import sys
