@@ -182,6 +182,19 @@ def gen_frames():
          image=res.image)
 
 
+def gen_dynamic():
+    # config 5 (dynamic scene): two frames of the 60-frame sequence -- objects rotated by different
+    # amounts about y and the point light elsewhere on its orbit -- at 1/400 of the pixels
+    for f in (7, 38):
+        spec = cfgs.config5_frame(f, width=100, height=40)
+        scene, cam, lights, cfg = ref_scene(spec)
+        res = pipeline.compose_frame(scene, cam, lights, cfg)
+        b = res.buffers
+        planes = np.stack([b.per_object_depth[i.id] for i in scene])
+        save(f"frame_config5_f{f}_100x40.npz", depth=b.depth, id=b.id, rgb=b.rgb, shadow=b.shadow,
+             image=res.image, planes=planes)
+
+
 def gen_analytic():
     """Oracle-backend scene (sphere tracing) from the reference's own shadow
     test (test_pipeline.py:211-217), plus a voxel radiance probe."""
@@ -308,6 +321,7 @@ def gen_train():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["geometry", "models", "forward", "analytic", "frames", "extra", "imgio", "train"]
+    which = sys.argv[1:] or ["geometry", "models", "forward", "analytic", "frames", "dynamic", "extra", "imgio",
+                             "train"]
     for w in which:
         globals()[f"gen_{w}"]()

@@ -90,7 +90,9 @@ def test_config1_step1_matches_reference(nedf, golden, prec):
 
 @pytest.mark.parametrize("prec", PRECISIONS)
 @pytest.mark.parametrize("fname,spec_fn", [("frame_config4_200x80.npz", lambda: CF.config4(200, 80)),
-                                           ("frame_config3_160x64.npz", lambda: CF.config3(160, 64))])
+                                           ("frame_config3_160x64.npz", lambda: CF.config3(160, 64)),
+                                           ("frame_config5_f7_100x40.npz", lambda: CF.config5_frame(7, width=100, height=40)),
+                                           ("frame_config5_f38_100x40.npz", lambda: CF.config5_frame(38, width=100, height=40))])
 def test_small_frames_match_reference(nedf, golden, fname, spec_fn, prec):
     z = golden(fname)
     spec = spec_fn()

@@ -90,7 +90,9 @@ def test_frame_config1(golden):
 
 
 @pytest.mark.parametrize("fname,spec", [("frame_config4_200x80.npz", C.config4(200, 80)),
-                                        ("frame_config3_160x64.npz", C.config3(160, 64))])
+                                        ("frame_config3_160x64.npz", C.config3(160, 64)),
+                                        ("frame_config5_f7_100x40.npz", C.config5_frame(7, width=100, height=40)),
+                                        ("frame_config5_f38_100x40.npz", C.config5_frame(38, width=100, height=40))])
 def test_frame_small_configs(golden, fname, spec):
     z = golden(fname)
     objs, cam, lights, cfg = oracle_scene(spec)
