@@ -463,11 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
         trace_at(tr, 420 + pt);
         {
           const uint32_t taddr = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + kAQCol + 32 * (pt & 3);
-          uint32_t lo[16], hi[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) { lo[j] = packed[j]; hi[j] = packed[16 + j]; }
-          tc::tmem_st16(taddr, lo);
-          tc::tmem_st16(taddr + 16, hi);
+          tc::tmem_st32(taddr, packed);
           tc::tmem_st_wait();
         }
         tc::tc_fence_before();
