@@ -63,7 +63,8 @@ enum {
   NEDF_OPT_GUARD_PPM = 2,       /* near-tie guard threshold tau, parts per million of max|logit| */
   NEDF_OPT_TC_CTAS = 3,         /* persistent CTAs for the tensor-core kernel (0 = one per SM) */
   NEDF_OPT_PROFILE = 4,         /* 1 = time every network launch with CUDA events (read back by nedf_read_stats) */
-  NEDF_OPT_TC_KERNEL = 5        /* one of NEDF_TC_*: which tensor-core network kernel runs */
+  NEDF_OPT_TC_KERNEL = 5,       /* one of NEDF_TC_*: which tensor-core network kernel runs */
+  NEDF_OPT_GUARD_CLUSTER = 6    /* near-tie guard kernel's cluster size: 4, 8, or 0 = by frame size */
 };
 
 /* Tensor-core network kernels (NEDF_OPT_TC_KERNEL). */

@@ -24,7 +24,7 @@ NEDF_ERR_UNSUPPORTED = -4
 NEDF_ERR_NOMEM = -5
 
 PREC_AUTO, PREC_TENSOR, PREC_FP32 = 0, 1, 2
-OPT_PRECISION, OPT_GUARD_PPM, OPT_TC_CTAS, OPT_PROFILE, OPT_TC_KERNEL = 1, 2, 3, 4, 5
+OPT_PRECISION, OPT_GUARD_PPM, OPT_TC_CTAS, OPT_PROFILE, OPT_TC_KERNEL, OPT_GUARD_CLUSTER = 1, 2, 3, 4, 5, 6
 TC_AUTO, TC_SINGLE, TC_PAIR, TC_MCAST2, TC_MCAST4 = 0, 1, 2, 3, 4
 
 FIELD_SPHERE, FIELD_BOX, FIELD_TORUS, FIELD_PLANE, FIELD_UNION, FIELD_TRANSFORMED, FIELD_VOXEL = range(1, 8)

@@ -60,6 +60,7 @@ struct NedfModel {
   float* bias_pack = nullptr;
   float* wstream = nullptr;
   float* wcluster = nullptr;
+  float* wcluster8 = nullptr;
   int device = 0;
 };
 
@@ -72,6 +73,7 @@ struct NedfContext {
   int guard_ppm = 3000;
   int tc_ctas = 0;
   int tc_kernel = NEDF_TC_AUTO;
+  int guard_cluster = 0;
   int profile = 0;
   int64_t launches = 0;
   // event pairs around network launches (NEDF_OPT_PROFILE); kind 0 = main, 1 = guard
@@ -413,7 +415,12 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
     if ((rc = prof_mark(ctx, st, 0, false))) return rc;
     if (a.use_guard) {
       if ((rc = prof_mark(ctx, st, 1, true))) return rc;
-      LAUNCH(ctx, launch_mlp_fp32_cluster(F.gt, F.redo, job, out, ctx->n_sms, st));
+      // 8-CTA clusters halve the MMA work per layer on a CTA's critical path but only ~18 fit at
+      // once (vs ~33 of 4): by default they take frames with at most half a 2000 x 800 x 8-object
+      // frame's (pixel, object) pairs, whose guard batch then still fits one round
+      int cl = ctx->guard_cluster;
+      if (cl == 0) cl = (int64_t)F.n_pix * F.sc.n_objs <= 6400000 ? 8 : 4;
+      LAUNCH(ctx, launch_mlp_fp32_cluster(F.gt, F.redo, job, out, ctx->n_sms, cl, st));
       if ((rc = prof_mark(ctx, st, 1, false))) return rc;
     }
     add_counts_kernel<<<1, 32, 0, st>>>(F.ls.count, F.redo.count, F.gt.n_groups, F.fj.stats, a.use_guard);
@@ -586,6 +593,10 @@ int nedf_set_option(NedfContext* c, int key, int64_t v) {
       if (v < NEDF_TC_AUTO || v > NEDF_TC_MCAST4) return fail(NEDF_ERR_INVALID, "bad tensor-core kernel");
       c->tc_kernel = (int)v;
       return NEDF_OK;
+    case NEDF_OPT_GUARD_CLUSTER:
+      if (v != 0 && v != 4 && v != 8) return fail(NEDF_ERR_INVALID, "guard cluster size must be 0, 4 or 8");
+      c->guard_cluster = (int)v;
+      return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }
@@ -598,6 +609,7 @@ int nedf_get_option(NedfContext* c, int key, int64_t* v) {
     case NEDF_OPT_TC_CTAS: *v = c->tc_ctas; return NEDF_OK;
     case NEDF_OPT_PROFILE: *v = c->profile; return NEDF_OK;
     case NEDF_OPT_TC_KERNEL: *v = c->tc_kernel; return NEDF_OK;
+    case NEDF_OPT_GUARD_CLUSTER: *v = c->guard_cluster; return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }
@@ -720,6 +732,7 @@ int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* 
     if (m->bias_pack) cudaFree(m->bias_pack);
     if (m->wstream) cudaFree(m->wstream);
     if (m->wcluster) cudaFree(m->wcluster);
+    if (m->wcluster8) cudaFree(m->wcluster8);
     if (m->dev) cudaFree(m->dev);
     delete m;
   };
@@ -742,9 +755,12 @@ int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* 
     e = fp32_pack_stream(params, info->d_in, F, info->n_blocks, info->n_coarse, info->n_fine, &m->wstream);
     if (e != cudaSuccess) { cleanup(); return fail(NEDF_ERR_CUDA, std::string("fp32 pack: ") + cudaGetErrorString(e)); }
     h.wstream = m->wstream;
-    e = fp32_pack_cluster(params, info->d_in, F, info->n_blocks, info->n_coarse, info->n_fine, &m->wcluster);
+    e = fp32_pack_cluster(params, info->d_in, F, info->n_blocks, info->n_coarse, info->n_fine, 4, &m->wcluster);
+    if (e == cudaSuccess)
+      e = fp32_pack_cluster(params, info->d_in, F, info->n_blocks, info->n_coarse, info->n_fine, 8, &m->wcluster8);
     if (e != cudaSuccess) { cleanup(); return fail(NEDF_ERR_CUDA, std::string("fp32 pack: ") + cudaGetErrorString(e)); }
     h.wcluster = m->wcluster;
+    h.wcluster8 = m->wcluster8;
     h.tensor_ok = 1;
   }
   e = cudaMalloc(&m->dev, sizeof(DevModel));
@@ -792,6 +808,7 @@ void nedf_model_free(NedfModel* m) {
   if (m->bias_pack) cudaFree(m->bias_pack);
   if (m->wstream) cudaFree(m->wstream);
   if (m->wcluster) cudaFree(m->wcluster);
+  if (m->wcluster8) cudaFree(m->wcluster8);
   if (m->dev) cudaFree(m->dev);
   delete m;
 }

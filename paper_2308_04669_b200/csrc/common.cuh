@@ -36,7 +36,8 @@ struct DevModel {
   const __half* wpack;           // tcgen05 operand image (see mlp_tc.cu)
   const float* bias_pack;        // tcgen05 bias image (fp32, padded to 256 per layer)
   const float* wstream;          // fp32 stream image for mlp_fp32s.cu (paper-shaped models)
-  const float* wcluster;         // fp32 cluster-split image for mlp_fp32c.cu (paper-shaped models)
+  const float* wcluster;         // fp32 cluster-split images for mlp_fp32c.cu (paper-shaped models):
+  const float* wcluster8;        //   4-CTA and 8-CTA clusters
   int64_t wT_off[40];            // layer offsets into wT  (n_layers <= 35 for the paper profile; general cap 40)
   int64_t b_off[40];
   int n_layers;

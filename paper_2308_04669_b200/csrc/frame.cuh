@@ -47,10 +47,11 @@ cudaError_t launch_mlp_fp32(const GroupTable& gt, const ListSet& ls, const RayJo
 cudaError_t launch_mlp_fp32_stream(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
                                    int n_sms, int rays_per_cta, cudaStream_t stream);
 // cluster-split fp32 network (mlp_fp32c.cu) for the guard's small batches
+// (cluster = 4 or 8 CTAs; the image must have been packed for the same cluster size)
 cudaError_t launch_mlp_fp32_cluster(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
-                                    int n_sms, cudaStream_t stream);
+                                    int n_sms, int cluster, cudaStream_t stream);
 cudaError_t fp32_pack_cluster(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
-                              float** dev);
+                              int cluster, float** dev);
 cudaError_t fp32_pack_stream(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
                              float** dev);
 

@@ -45,8 +45,6 @@
 namespace nedf {
 namespace {
 
-constexpr int kC = 4;                 // CTAs per cluster
-constexpr int kCols = 256 / kC;       // output columns per CTA (64): 8 warps x 8
 constexpr int kThreads = 256;         // compute threads (8 warps)
 constexpr int kBlock = kThreads + 32; // + the weight producer warp
 constexpr int kR = 16;                // rays per cluster tile (the MMA M dimension)
@@ -58,22 +56,35 @@ constexpr int kHeadStages = kHeadK / (8 * kKSteps);   // 8
 constexpr int kBodyStages = 256 / (8 * kKSteps);      // 2
 constexpr int kLayers = 34;           // head, 32 block layers, fused tail
 constexpr int kStagesPerTile = kHeadStages + (kLayers - 1) * kBodyStages;       // 74
-constexpr uint32_t kStageBytes = 8 * kKSteps * 32 * 8;                         // 32 KB
 constexpr int kRing = 3;
-constexpr size_t kImageFloats = (size_t)kStagesPerTile * kC * (kStageBytes / 4);
 
+// Cluster shapes: KC = 4 CTAs x 64 output columns (8 column groups of 8, one warp each, whole K),
+// or KC = 8 CTAs x 32 columns (4 column groups, two warps each splitting K) -- half the MMA work
+// per layer on a CTA's critical path for frames whose guard batch fits 8-CTA clusters in one round.
+template <int KC>
+struct Cfg {
+  static constexpr int kC = KC;
+  static constexpr int kCols = 256 / KC;              // output columns per CTA
+  static constexpr int kNG = kCols / 8;               // column groups (one MMA n-tile each)
+  static constexpr int kKP = 8 / kNG;                 // K parts per column group (warps)
+  static constexpr uint32_t kStageBytes = kNG * kKSteps * 32 * 8;   // 32 KB / 16 KB
+  static constexpr uint32_t kPeerBytes = (KC - 1) * kR * kCols * 4; // the peers' columns of one layer
+  static constexpr size_t kImageFloats = (size_t)kStagesPerTile * KC * (kStageBytes / 4);
+};
+
+template <int KC>
 struct ClSmem {
-  float2 ring[kRing][kStageBytes / 8];   // weight stage slots: [warp][k-step][lane] (W[n][k], W[n][k + 4])
+  float2 ring[kRing][Cfg<KC>::kStageBytes / 8];   // weight stage slots: [column group][k-step][lane] (W[n][k], W[n][k + 4])
   float f[kR][kFStride];
   float x[kR][kXStride];
   float h[kR][kXStride];
   double ray[kR][8];
   uint32_t pix[kR], obj[kR];
   int valid[kR];
+  float4 part[8][32];            // KC = 8: the second K part's partial fragments, per column group and lane
   uint64_t full[kRing], empty[kRing];
-  uint64_t layer_bar[2];         // layer L outputs on layer_bar[L & 1]: 12 KB from the 3 peers + the 8 local warps' arrivals
+  uint64_t layer_bar[2];         // layer L outputs on layer_bar[L & 1]: the peers' bytes + the local finishing warps' arrivals
 };
-constexpr uint32_t kPeerBytes = (kC - 1) * kR * kCols * 4;   // 12 KB: the peers' columns of one layer
 
 // remote store that completes its bytes on the receiving CTA's mbarrier
 __device__ __forceinline__ void st_async_v4(uint32_t addr, float a, float b, float c, float d, uint32_t mbar) {
@@ -105,10 +116,14 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], 
 __device__ unsigned long long g_cl_trace[256];
 __device__ int g_cl_trace_on;
 
-__global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kBlock, 1)
+template <int KC>
+__global__ void __cluster_dims__(KC, 1, 1) __launch_bounds__(kBlock, 1)
 mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
+  using G = Cfg<KC>;
+  constexpr int kC = KC, kCols = G::kCols, kNG = G::kNG, kKP = G::kKP;
+  constexpr uint32_t kStageBytes = G::kStageBytes;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  ClSmem& S = *reinterpret_cast<ClSmem*>(smem_raw);
+  ClSmem<KC>& S = *reinterpret_cast<ClSmem<KC>*>(smem_raw);
   __shared__ int s_tiles[65];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -124,9 +139,10 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       cum += (ls.count[g] + kR - 1) / kR;
       s_tiles[g + 1] = cum;
     }
-    for (int i = 0; i < kRing; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], 8); }
-    tc::mbar_init(&S.layer_bar[0], 1 + 8);     // tid 0's expect_tx + one arrival per compute warp
-    tc::mbar_init(&S.layer_bar[1], 1 + 8);
+    // a stage is consumed by the kNG warps of one K part; a layer is finished by kNG warps
+    for (int i = 0; i < kRing; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], kNG); }
+    tc::mbar_init(&S.layer_bar[0], 1 + kNG);   // tid 0's expect_tx + one arrival per finishing warp
+    tc::mbar_init(&S.layer_bar[1], 1 + kNG);
     tc::mbar_fence_init();
   }
   tc::cluster_sync();           // peers' barriers initialised before anyone stores into them
@@ -142,7 +158,8 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
     for (int t = cid; t < total; t += n_cl) {
       int g = 0;
       while (g < ng - 1 && t >= s_tiles[g + 1]) ++g;
-      const unsigned char* img = reinterpret_cast<const unsigned char*>(gt.models[g].wcluster);
+      const unsigned char* img =
+          reinterpret_cast<const unsigned char*>(KC == 8 ? gt.models[g].wcluster8 : gt.models[g].wcluster);
       for (int q = 0; q < kStagesPerTile; ++q, ++gq) {
         const int slot = gq % kRing;
         if (lane == 0) {
@@ -162,7 +179,8 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
 
   // ------------------------------------------------------------------ compute warps
   const int gid = lane >> 2, tig = lane & 3;          // MMA fragment coordinates
-  const int col = kCols * (int)rank + 8 * warp + 2 * tig;   // this lane's two output columns: col, col + 1
+  const int ngw = warp % kNG, kpart = warp / kNG;    // column group, K part (stages alternate K parts)
+  const int col = kCols * (int)rank + 8 * ngw + 2 * tig;    // this lane's two output columns: col, col + 1
   // shared::cluster address of S in every CTA of the cluster
   uint32_t peer[kC];
 #pragma unroll
@@ -255,16 +273,16 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       for (int i = 0; i < 12; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
       const float* a_lo_row = A + gid * lda + tig;           // rows gid, gid + 8; columns k0 + tig, k0 + tig + 4
       const float* a_hi_row = A + (gid + 8) * lda + tig;
-      for (int st = 0; st < nst; ++st) {
+      for (int st = 0; st < nst; ++st, ++gq) {
+        if (kKP > 1 && st % kKP != kpart) continue;
         // this warp's 16 k-steps of the stage, copied out of the ring slot, which is then released
         const int slot = gq % kRing;
         const long long tw0 = (tr && L == 5) ? clock64() : 0;
         tc::mbar_wait(&S.full[slot], (gq / kRing) & 1);
         if (tr && L == 5) g_cl_trace[64 * ti + 43] += clock64() - tw0;
-        ++gq;
         float2 wv[kKSteps];
 #pragma unroll
-        for (int ks = 0; ks < kKSteps; ++ks) wv[ks] = S.ring[slot][(warp * kKSteps + ks) * 32 + lane];
+        for (int ks = 0; ks < kKSteps; ++ks) wv[ks] = S.ring[slot][(ngw * kKSteps + ks) * 32 + lane];
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&S.empty[slot]);
 #pragma unroll
@@ -288,6 +306,20 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       for (int i = 0; i < 4; ++i)
         c[i] = (((acc[0][i] + acc[3][i]) + (acc[6][i] + acc[9][i])) + ((acc[1][i] + acc[4][i]) + (acc[7][i] + acc[10][i]))) +
                ((acc[2][i] + acc[5][i]) + (acc[8][i] + acc[11][i]));
+      if (kKP > 1) {
+        // the second K part hands its partial fragment to its column group's first (a named barrier
+        // per pair), which finishes the layer; the buffer is rewritten only after this layer's exchange
+        if (kpart == 1) {
+          S.part[ngw][lane] = make_float4(c[0], c[1], c[2], c[3]);
+          tc::named_bar_arrive(2 + ngw, 64);
+          tc::mbar_wait(&S.layer_bar[layer_count & 1], (layer_count >> 1) & 1);
+          ++layer_count;
+          continue;
+        }
+        tc::named_bar(2 + ngw, 64);
+        const float4 pp = S.part[ngw][lane];
+        c[0] += pp.x; c[1] += pp.y; c[2] += pp.z; c[3] += pp.w;
+      }
       if (tr && L == 5) g_cl_trace[64 * ti + 41] = clock64();
       // epilogue: rows gid / gid + 8, columns col / col + 1 (c0 c1 / c2 c3)
       float v[4];
@@ -326,7 +358,7 @@ mlp_fp32_cluster_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&S.layer_bar[lb]);
       if (tr && L == 5) g_cl_trace[64 * ti + 42] = clock64();
-      if (tid == 0) tc::mbar_expect_tx(&S.layer_bar[lb], kPeerBytes);
+      if (tid == 0) tc::mbar_expect_tx(&S.layer_bar[lb], G::kPeerBytes);
       tc::mbar_wait(&S.layer_bar[lb], (layer_count >> 1) & 1);
       ++layer_count;
       if (tr) g_cl_trace[64 * ti + 3 + L] = clock64();
@@ -374,38 +406,47 @@ extern "C" int nedf_diag_cl_trace(int enable, unsigned long long* out, int n) {
 
 namespace nedf {
 
-cudaError_t launch_mlp_fp32_cluster(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
-                                    int n_sms, cudaStream_t stream) {
+template <int KC>
+cudaError_t launch_guard(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out, int n_sms,
+                         cudaStream_t stream) {
   static int max_clusters = 0;
-  const size_t smem = sizeof(ClSmem);
+  const size_t smem = sizeof(ClSmem<KC>);
   if (max_clusters == 0) {
-    cudaError_t e = cudaFuncSetAttribute(mlp_fp32_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(mlp_fp32_cluster_kernel<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kC * (n_sms / kC), 1, 1);
+    cfg.gridDim = dim3(KC * (n_sms / KC), 1, 1);
     cfg.blockDim = dim3(kBlock, 1, 1);
     cfg.dynamicSmemBytes = smem;
     int n = 0;
-    e = cudaOccupancyMaxActiveClusters(&n, mlp_fp32_cluster_kernel, &cfg);
+    e = cudaOccupancyMaxActiveClusters(&n, mlp_fp32_cluster_kernel<KC>, &cfg);
     if (e != cudaSuccess) return e;
     max_clusters = n > 0 ? n : 1;
-    if (getenv("NEDF_VERBOSE")) fprintf(stderr, "nedf: fp32 cluster kernel, %d co-resident clusters\n", n);
+    if (getenv("NEDF_VERBOSE")) fprintf(stderr, "nedf: fp32 cluster kernel x%d, %d co-resident clusters\n", KC, n);
   }
-  mlp_fp32_cluster_kernel<<<kC * max_clusters, kBlock, smem, stream>>>(gt, ls, job, out);
+  mlp_fp32_cluster_kernel<KC><<<KC * max_clusters, kBlock, smem, stream>>>(gt, ls, job, out);
   return cudaGetLastError();
 }
 
-// Cluster image, streamed as 32 KB stages: stage q (head K block q < 8, then
-// layer L = 1 + (q - 8) / 2, K block j = (q - 8) % 2), CTA r -> float2
-// [(q kC + r) 4096 + (16 w + s) 32 + lane] = (W[n][k], W[n][k + 4]) for warp w,
-// k-step s, lane = 4 gid + tig: output column n = 64 r + 8 w + gid, K row
-// k = 128 j + 8 s + tig (the B fragment of an m16n8k8 MMA).  Head rows are the
-// 16 points' 63 features + 1 zero; tail outputs: fine 0-127, coarse 128-191,
-// alpha 192, zero padding.
-cudaError_t fp32_pack_cluster(const float* P, int d_in, int F, int n_blocks, int n_coarse, int n_fine, float** dev) {
+cudaError_t launch_mlp_fp32_cluster(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
+                                    int n_sms, int cluster, cudaStream_t stream) {
+  return cluster == 8 ? launch_guard<8>(gt, ls, job, out, n_sms, stream)
+                      : launch_guard<4>(gt, ls, job, out, n_sms, stream);
+}
+
+// Cluster image for KC-CTA clusters, streamed as stages of 128 K rows: stage q
+// (head K block q < 8, then layer L = 1 + (q - 8) / 2, K block j = (q - 8) % 2),
+// CTA r -> float2 [(q KC + r) (kStageBytes / 8) + (16 w + s) 32 + lane] =
+// (W[n][k], W[n][k + 4]) for column group w, k-step s, lane = 4 gid + tig:
+// output column n = (256 / KC) r + 8 w + gid, K row k = 128 j + 8 s + tig (the B
+// fragment of an m16n8k8 MMA).  Head rows are the 16 points' 63 features + 1
+// zero; tail outputs: fine 0-127, coarse 128-191, alpha 192, zero padding.
+template <int KC>
+cudaError_t pack_guard(const float* P, int d_in, int F, int n_blocks, int n_coarse, int n_fine, float** dev) {
+  using G = Cfg<KC>;
   if (F != 256 || n_blocks != 16 || d_in != kDin || n_coarse != 64 || n_fine != 128) return cudaErrorInvalidValue;
-  std::vector<float> img(kImageFloats, 0.f);
+  std::vector<float> img(G::kImageFloats, 0.f);
   size_t p = 0;
   const float* Wh = P + p; p += (size_t)F * d_in + F;
   std::vector<const float*> Wl(32);
@@ -425,13 +466,14 @@ cudaError_t fp32_pack_cluster(const float* P, int d_in, int F, int n_blocks, int
   for (int q = 0; q < kStagesPerTile; ++q) {
     const int L = q < kHeadStages ? 0 : 1 + (q - kHeadStages) / kBodyStages;
     const int j = q < kHeadStages ? q : (q - kHeadStages) % kBodyStages;
-    for (int r = 0; r < kC; ++r)
-      for (int w = 0; w < 8; ++w)
+    for (int r = 0; r < KC; ++r)
+      for (int w = 0; w < G::kNG; ++w)
         for (int s = 0; s < kKSteps; ++s)
           for (int lane = 0; lane < 32; ++lane) {
-            const int n = kCols * r + 8 * w + (lane >> 2);
+            const int n = G::kCols * r + 8 * w + (lane >> 2);
             const int k = 8 * kKSteps * j + 8 * s + (lane & 3);
-            float* dst = img.data() + 2 * (((size_t)q * kC + r) * (kStageBytes / 8) + (size_t)(w * kKSteps + s) * 32 + lane);
+            float* dst = img.data() +
+                         2 * (((size_t)q * KC + r) * (G::kStageBytes / 8) + (size_t)(w * kKSteps + s) * 32 + lane);
             dst[0] = w_of(L, n, k);
             dst[1] = w_of(L, n, k + 4);
           }
@@ -439,6 +481,12 @@ cudaError_t fp32_pack_cluster(const float* P, int d_in, int F, int n_blocks, int
   cudaError_t e = cudaMalloc(dev, img.size() * sizeof(float));
   if (e == cudaSuccess) e = cudaMemcpy(*dev, img.data(), img.size() * sizeof(float), cudaMemcpyHostToDevice);
   return e;
+}
+
+cudaError_t fp32_pack_cluster(const float* P, int d_in, int F, int n_blocks, int n_coarse, int n_fine, int cluster,
+                              float** dev) {
+  return cluster == 8 ? pack_guard<8>(P, d_in, F, n_blocks, n_coarse, n_fine, dev)
+                      : pack_guard<4>(P, d_in, F, n_blocks, n_coarse, n_fine, dev);
 }
 
 }  // namespace nedf

@@ -246,6 +246,10 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+// producer side of a named barrier: arrive without waiting (the consumers use named_bar)
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
 template <uint32_t kRegs>
 __device__ __forceinline__ void reg_dealloc() {
