@@ -92,6 +92,12 @@ def main():
              "--set full -k regex:nedf_mlp_tc_kernel [--tc-kernel single]", "tc_single_full"),
             ("setup_full.ncu-rep", "setup_kernel", "--set full -k regex:setup_kernel", "setup")]:
         if (src / rep).exists() and (src / rep).stat().st_size > 0:
+            if out != "tc":      # full-set captures: also the section details (rules, speed-of-light, stalls)
+                det = subprocess.run(["ncu", "-i", str(src / rep), "--page", "details", "--csv"], capture_output=True,
+                                     text=True).stdout
+                if det:
+                    name = "tc_single" if out == "tc_single_full" else out
+                    (dst / f"{p}_{name}_kernel_details.csv").write_text(det)
             try:
                 s = rep_summary(src / rep, kern, f"ncu {cap} --clock-control none -s 2 -c 1 {base}",
                                 "STEP-1 launch of a config-4 frame")
