@@ -1,37 +1,39 @@
-// fp32-accurate network for small ray batches, split across a cluster of
-// kC = 4 CTAs, on the warp-level tensor cores (mma.sync, 3xTF32).
+// fp32-accurate network for small ray batches, split across a cluster of KC
+// CTAs (4 or 8), on the warp-level tensor cores (mma.sync, 3xTF32).
 //
 // Role: the near-tie guard's re-evaluation (a few hundred rays per frame).
 // Its cost is latency, not FLOPs: one ray still walks a 35-layer chain.  The
-// 4 CTAs of a cluster share a 16-ray tile: CTA r owns output columns
-// [64 r, 64 r + 64) of every layer, so it needs only its 1/4 of the weights,
-// and scatters its outputs into every peer's activation buffer with st.async
-// through distributed shared memory.  Each store completes transaction bytes
-// on the receiving CTA's mbarrier, so a CTA starts layer L+1 as soon as all
-// 16 KB of layer L have landed -- no cluster-wide barrier per layer.  Buffer
-// reuse is safe without one: a warp sends its layer-L outputs only after its
-// layer-L MMAs, so once every layer-L output has landed anywhere, every warp
-// of the cluster is done reading the buffer layer L+1 overwrites.  Two layer
-// barriers alternate so a peer one layer ahead never completes the current
-// phase.
+// KC CTAs of a cluster share a 16-ray tile: CTA r owns output columns
+// [(256 / KC) r, (256 / KC) (r + 1)) of every layer, so it needs only its
+// 1/KC of the weights, and sends its outputs into every peer's activation
+// buffer with st.async through distributed shared memory.  Each store completes
+// transaction bytes on the receiving CTA's mbarrier, so a CTA starts layer L+1
+// as soon as all 16 KB of layer L have landed -- no cluster-wide barrier per
+// layer.  Buffer reuse is safe without one: a warp sends its layer-L outputs
+// only after its layer-L MMAs, so once every layer-L output has landed
+// anywhere, every warp of the cluster is done reading the buffer layer L+1
+// overwrites.  Two layer barriers alternate so a peer one layer ahead never
+// completes the current phase.
 //
-// Arithmetic: warp w of a CTA owns 8 output columns and the whole K range of
-// every layer, so a layer is 16 rays x 8 columns x K per warp with no
-// cross-warp reduction: m16n8k8 TF32 MMAs with fp32 accumulation, each
-// operand split into a TF32 high part and a TF32 remainder and three products
-// accumulated (a_lo b_hi + a_hi b_lo + a_hi b_hi; the dropped a_lo b_lo term
-// is ~2^-20 of a product), i.e. near-fp32 accuracy on the tensor pipe.  A
-// 16 x 64 x 256 layer slice takes ~3.4k cycles of HMMA (ncu: "math" throttle
-// on the MMA pipe; scripts/cl_trace.py) against ~4.2k for the same slice as
-// FFMA2 (the previous version of this kernel); the split runs on LOP3/FADD,
-// since cvt.rna.tf32 issues at a quarter rate.
-// Float64 features (sincospi), float32 weights and activations.
+// Arithmetic: a CTA's columns form 8-column groups (one m16n8 n-tile each):
+// with KC = 4, warp w owns group w and the whole K range; with KC = 8, two warps
+// share a group, taking alternate weight stages (K halves), and the second
+// hands its partial fragment to the first through shared memory and a named
+// barrier.  m16n8k8 TF32 MMAs with fp32 accumulation, each operand split into a
+// TF32 high part and a TF32 remainder and three products accumulated (a_lo b_hi
+// + a_hi b_lo + a_hi b_hi; the dropped a_lo b_lo term is ~2^-20 of a product),
+// i.e. near-fp32 accuracy on the tensor pipe.  A 16 x 64 x 256 layer slice takes
+// ~3.4k cycles of HMMA (ncu: "math" throttle on the MMA pipe;
+// scripts/cl_trace.py) against ~4.2k for the same slice as FFMA2 (the previous
+// version of this kernel); the split runs on LOP3/FADD, since cvt.rna.tf32
+// issues at a quarter rate.  Float64 features (sincospi and double-angle
+// steps), float32 weights and activations.
 //
 // Weights: a producer warp (warp 8) streams the CTA's slice of the image as
-// 32 KB stages (128 K rows x 64 columns; the head is 8 stages, every later
-// layer 2) through a 3-slot shared-memory ring with bulk copies; a compute
-// warp copies its part of a stage into registers and releases the slot
-// before its MMAs.
+// stages of 128 K rows (32 KB for KC = 4, 16 KB for KC = 8; the head is 8
+// stages, every later layer 2) through a 3-slot shared-memory ring with bulk
+// copies; a compute warp copies its part of a stage into registers and
+// releases the slot before its MMAs.
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
