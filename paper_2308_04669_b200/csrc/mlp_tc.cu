@@ -349,20 +349,29 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
           const uint64_t b0 = dring + stage * kSlotDesc;
           if (tc::elect_one()) {
             if (pend >= 0) tc::mma_commit_mc(&S.empty[pend], cmask);
+            if (c < 15) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) tc::mma_ts(tbase + kAccCol, a0 + 8 * k, b0 + 2 * k, id256, (c | k) ? 1u : 0u);
-            tc::mma_commit_mc(&S.empty[stage], cmask);        // releases slots stage, stage + 1 and the point
+              for (int k = 0; k < 4; ++k)
+                tc::mma_ts(tbase + kAccCol, a0 + 8 * k, b0 + 2 * k, id256, (c | k) ? 1u : 0u);
+              tc::mma_commit_mc(&S.empty[stage], cmask);      // releases slots stage, stage + 1 and the point
+            } else {
+              // last point as two N = 128 halves: slice 0 completes half a point earlier, so its
+              // epilogue (which layer 1's first MMAs wait for) overlaps slice 1's last MMAs
+#pragma unroll
+              for (int k = 0; k < 4; ++k) tc::mma_ts(tbase + kAccCol, a0 + 8 * k, b0 + 2 * k, id128, 1u);
+              tc::mma_commit(&S.acc_full[0]);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                tc::mma_ts(tbase + kAccCol + 128, a0 + 8 * k, b0 + kSlotDesc + 2 * k, id128, 1u);
+              tc::mma_commit_mc(&S.empty[stage], cmask);
+              tc::mma_commit(&S.acc_full[1]);
+            }
           }
           __syncwarp();
           pend = -1;
           stage += 2;
           if (stage == kStages) { stage = 0; phase ^= 1; }
         }
-        if (tc::elect_one()) {
-          tc::mma_commit(&S.acc_full[0]);
-          tc::mma_commit(&S.acc_full[1]);
-        }
-        __syncwarp();
         trace_at(tr, 40);
         if (tr) g_tc_trace[603] = w_full;        // weight waits during the head alone
         ++layer_ctr;
