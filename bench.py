@@ -8,9 +8,10 @@ A step is one full frame (STEP 1 depth/id, STEP 2 shading, STEP 3 shadows,
 composite) rendered by `nedf_render_frame` through the C ABI with the scene
 resident on the GPU (`value`), and again through the public Python API
 `compose_frame` with the result copied to pinned host memory (`e2e`).  For
-N > 1 (torchrun) each rank renders interleaved 16-row stripes and the tiles
-are gathered to rank 0 over NCCL inside the timed region; time is the max over
-ranks of CUDA-event time.  L2 is flushed (256 MiB write) before every timed
+N > 1 (`--gpus N` re-runs itself under torch.distributed.run, one rank per GPU)
+each rank renders every N-th camera row and the tiles are gathered to rank 0
+over NCCL inside the timed region; time is the max over ranks of CUDA-event
+time.  L2 is flushed (256 MiB write) before every timed
 frame, outside its event bracket.
 
 `--impl reference` times the reference algorithm (the float64 oracle port,
@@ -44,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="auto", choices=["auto", "tensor", "fp32"])
-    ap.add_argument("--tc-kernel", default="auto", choices=["auto", "single", "pair", "mcast2", "mcast4"])
+    ap.add_argument("--tc-kernel", default="auto", choices=["auto", "single", "mcast2", "mcast4"])
     ap.add_argument("--width", type=int, default=2000)
     ap.add_argument("--height", type=int, default=800)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -67,6 +68,27 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def relaunch(args) -> int:
+    """`--gpus N` (N > 1) outside torchrun: re-run this script as N ranks, one
+    process per GPU (torch.distributed.run on 127.0.0.1); rank 0 prints the line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def bench_config(spec, world: int) -> dict:
+    """`config` of both arms' JSON lines (same keys, so the driver can pair them)."""
+    return {"workload": "config4: 8-object NeDF scene, 2000x800, point-light shadows",
+            "objects": len(spec.objects), "width": spec.camera.width, "height": spec.camera.height,
+            "parallelism": f"1-row interleaved image tiles x{world}, gather to rank 0" if world > 1 else "single GPU",
+            "l2": "flushed (256 MiB write) before every timed frame"}
 
 
 def peaks():
@@ -119,8 +141,7 @@ def run_reference(args):
         "metric": METRIC, "value": ms, "unit": "ms/frame", "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config4: 8-object NeDF scene, 2000x800, point-light shadows",
-                   "objects": 8, "width": args.width, "height": args.height},
+        "config": bench_config(spec, args.gpus),
         "cpu_baseline": {"value": ms, "unit": "ms/frame", "cores": threads, "kind": "port",
                          "sample": f"every {step}th row and column ({npx} px), extrapolated x{full / npx:.0f}; "
                                    f"{ev} NeDF evaluations per sample"},
@@ -179,9 +200,13 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     import numpy as np
     import torch
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -191,13 +216,13 @@ def main():
 
     spec = CF.config4(args.width, args.height)
     scene, cam, lights, cfg = scenes.build(spec, device=local)
-    rows = D.stripe_rows(cam.height, rank, world) if world > 1 else None
+    rows = D.interleave_rows(cam.height, rank, world) if world > 1 else None
     ctx = _lib.context(local)
     ctx.set_option(_lib.OPT_PRECISION, {"auto": _lib.PREC_AUTO, "tensor": _lib.PREC_TENSOR,
                                         "fp32": _lib.PREC_FP32}[args.precision])
     ctx.set_option(_lib.OPT_PROFILE, 1)
     ctx.set_option(_lib.OPT_TC_KERNEL, {"auto": _lib.TC_AUTO, "single": _lib.TC_SINGLE,
-                                        "pair": _lib.TC_PAIR, "mcast2": _lib.TC_MCAST2,
+                                        "mcast2": _lib.TC_MCAST2,
                                         "mcast4": _lib.TC_MCAST4}[args.tc_kernel])
     buf = pipeline.FrameBuffers(cam.width, cam.height, device=local, rows=rows)
     rnd = pipeline.FrameRenderer(scene, cam, lights, cfg, buffers=buf)
@@ -313,8 +338,7 @@ def main():
     tflops = (evals * FLOP_PER_EVAL) / (net_ms * 1e-3) / 1e12 if net_ms > 0 else 0.0
     roofline = {"bound": "tensor", "achieved": tflops, "peak": burst, "unit": "TFLOP/s",
                 "frac": tflops / burst, "frac_sustained": tflops / sustained, "peak_source": src,
-                "kernel": ("nedf_mlp_tc2_kernel" if ctx.get_option(_lib.OPT_TC_KERNEL) == _lib.TC_PAIR else "nedf_mlp_tc_kernel")
-                if ctx.get_option(_lib.OPT_PRECISION) != _lib.PREC_FP32 else "mlp_fp32_stream_kernel",
+                "kernel": "nedf_mlp_tc_kernel" if ctx.get_option(_lib.OPT_PRECISION) != _lib.PREC_FP32 else "mlp_fp32_stream_kernel",
                 "kernel_ms_per_frame": net_ms, "guard_ms_per_frame": guard_ms,
                 "flop_per_eval": FLOP_PER_EVAL, "evals_per_launch": evals / max(1, st["net_launches"] / args.steps),
                 "traffic": traffic_per_launch(), "traffic_unit": "bytes (DRAM read + write per launch, ncu)"}
@@ -323,10 +347,7 @@ def main():
         "warmup": max(3, args.warmup), "ms_per_step": t_frame, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "fp16 tcgen05 (fp32 accum) + fp32 guard" if args.precision == "auto" else args.precision,
         "data": "synthetic (random-init paper-profile NeDFs, seeds 0/1/5)",
-        "config": {"workload": "config4: 8-object NeDF scene, 2000x800, point-light shadows",
-                   "objects": len(scene), "width": cam.width, "height": cam.height,
-                   "parallelism": f"image stripes x{world}" if world > 1 else "single GPU",
-                   "l2": "flushed (256 MiB write) before every timed frame"},
+        "config": bench_config(spec, world),
         "nedf_evals_per_frame": evals_all, "guarded_per_frame": guarded,
         "nedf_rays_per_s": evals_all / (t_frame * 1e-3),
         "gpu_launches": int(st["launches"]), "clocks": clocks, "roofline": roofline, "e2e": e2e,

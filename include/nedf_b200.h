@@ -71,7 +71,7 @@ enum {
 enum {
   NEDF_TC_AUTO = 0,    /* the fastest measured one (currently NEDF_TC_MCAST2) */
   NEDF_TC_SINGLE = 1,  /* one CTA per 128-ray tile, M = 128, own weight stream */
-  NEDF_TC_PAIR = 2,    /* CTA pairs (cta_group::2) per 256-ray tile, M = 256, half the weight stream per SM */
+  /* 2 is retired: the cta_group::2 variant (round 1) measured slower and was removed */
   NEDF_TC_MCAST2 = 3,  /* clusters of 2 CTAs (M = 128 each) sharing one multicast weight stream */
   NEDF_TC_MCAST4 = 4   /* clusters of 4 CTAs sharing one multicast weight stream */
 };

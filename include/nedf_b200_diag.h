@@ -21,11 +21,6 @@ extern "C" {
 int nedf_diag_umma(const void* a_dev, const void* b_dev, float* d_dev, int k, int n, int a_in_tmem, int d_col,
                    void* stream);
 
-/* CTA-pair form (cta_group::2, M = 256): D[256][N] = A[256][K] * B[N][K]^T,
- * N in {32,...,256} step 32; CTA r holds A rows [128r, 128r+128) and B rows
- * [r N/2, (r+1) N/2). */
-int nedf_diag_umma2(const void* a_dev, const void* b_dev, float* d_dev, int k, int n, int a_in_tmem, void* stream);
-
 /* Raw network logits for local rays (rows that miss the box are left
  * untouched): precision NEDF_PREC_TENSOR (tcgen05 kernel) or NEDF_PREC_FP32. */
 int nedf_diag_ray_logits(NedfContext* ctx, const NedfModel* m, const double* origins_dev, const double* dirs_dev,
@@ -39,13 +34,6 @@ int nedf_diag_ray_logits(NedfContext* ctx, const NedfModel* m, const double* ori
  * encoder point written / slot acquired, [450+L] producer layer start. */
 int nedf_diag_tc_trace(int enable, unsigned long long* out, int n);
 
-/* Wait accounting of cluster 0's second tile in the CTA-pair kernel (clock64
- * cycles, n <= 64): [0..3] MMA waits on full / peer_full / epi_done / enc_full,
- * [4] MMA tile cycles, [8+r] producer waits on empty (CTA r), [10] relay waits,
- * [12+r]/[14+r] encoder waits / tile cycles, [16+r]/[18+r] epilogue waits /
- * tile cycles. */
-int nedf_diag_tc2_trace(int enable, unsigned long long* out, int n);
-
 /* Timeline of cluster 0 / CTA 0 of the cluster-split fp32 guard kernel (clock64):
  * per tile i < 4, [64 i] start, [64 i + 1] rays set up, [64 i + 2] features
  * landed, [64 i + 3 + L] layer L landed, [64 i + 40] decoded; n <= 256. */
@@ -54,9 +42,6 @@ int nedf_diag_cl_trace(int enable, unsigned long long* out, int n);
 /* tcgen05 issue-rate probe: `iters` M=128 x N MMAs (ts: A from TMEM) from one
  * warp, committing every `per_commit`; writes elapsed clock64 cycles to out_dev. */
 int nedf_diag_mma_rate(int ts, int n, int iters, int per_commit, unsigned long long* out_dev);
-
-/* Same probe for the CTA-pair form (M = 256 x N, issued by the even CTA). */
-int nedf_diag_mma2_rate(int ts, int n, int iters, unsigned long long* out_dev);
 
 /* L2 -> shared memory bulk-copy bandwidth probe: `ctas` CTAs each stream `total`
  * bytes of `src` (wrapping within `span`) through `depth` x `stage`-byte

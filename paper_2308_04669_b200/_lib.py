@@ -25,7 +25,7 @@ NEDF_ERR_NOMEM = -5
 
 PREC_AUTO, PREC_TENSOR, PREC_FP32 = 0, 1, 2
 OPT_PRECISION, OPT_GUARD_PPM, OPT_TC_CTAS, OPT_PROFILE, OPT_TC_KERNEL, OPT_GUARD_CLUSTER = 1, 2, 3, 4, 5, 6
-TC_AUTO, TC_SINGLE, TC_PAIR, TC_MCAST2, TC_MCAST4 = 0, 1, 2, 3, 4
+TC_AUTO, TC_SINGLE, TC_MCAST2, TC_MCAST4 = 0, 1, 3, 4
 
 FIELD_SPHERE, FIELD_BOX, FIELD_TORUS, FIELD_PLANE, FIELD_UNION, FIELD_TRANSFORMED, FIELD_VOXEL = range(1, 8)
 DEPTH_NEDF, DEPTH_ANALYTIC = 0, 1
@@ -192,17 +192,33 @@ class Context:
                 "launches": s.launches, "net_launches": s.net_launches, "net_ms": s.net_ms,
                 "guard_ms": s.guard_ms, "h2d_bytes": s.h2d_bytes}
 
-    def snapshot_stats(self, stream) -> tuple[int, dict]:
+    _RESET_SLOT = 63                     # mapped slot 63 only absorbs resets; 0-62 rotate
+
+    def reset_stats(self, stream) -> None:
+        """Non-blocking: zero the device counters (their old values land in the reset slot)."""
+        s = NedfStepStats()
+        check(self._lib.nedf_stats_snapshot(self.handle, self._RESET_SLOT, C.byref(s), stream))
+
+    def snapshot_stats(self, stream) -> tuple[tuple[int, int], dict]:
         """Non-blocking: enqueue this step's counters into the next mapped slot; returns
-        (slot, host-side counters).  Resolve with `slot_stats(slot)` after the stream
-        passes this point.  64 slots rotate."""
-        slot = getattr(self, "_next_slot", 0)
-        self._next_slot = (slot + 1) % 64
+        (ticket, host-side counters).  Resolve with `slot_stats(ticket)` after the stream
+        passes this point; 63 slots rotate, and a ticket whose slot has been reused since
+        raises instead of returning another step's counters."""
+        seq = getattr(self, "_seq", 0)
+        self._seq = seq + 1
+        slot = seq % self._RESET_SLOT
+        if not hasattr(self, "_slot_owner"):
+            self._slot_owner = {}
+        self._slot_owner[slot] = seq
         s = NedfStepStats()
         check(self._lib.nedf_stats_snapshot(self.handle, slot, C.byref(s), stream))
-        return slot, {"launches": s.launches, "h2d_bytes": s.h2d_bytes}
+        return (slot, seq), {"launches": s.launches, "h2d_bytes": s.h2d_bytes}
 
-    def slot_stats(self, slot: int) -> dict:
+    def slot_stats(self, ticket) -> dict:
+        slot, seq = ticket
+        if self._slot_owner.get(slot) != seq:
+            raise RuntimeError(f"stats of step {seq} were overwritten: read them within "
+                               f"{self._RESET_SLOT} steps")
         s = NedfStepStats()
         check(self._lib.nedf_stats_slot(self.handle, slot, C.byref(s)))
         return {"evals": s.evals, "guarded": s.guarded, "covered": s.covered, "resampled": s.resampled}

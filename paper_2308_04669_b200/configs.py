@@ -145,17 +145,39 @@ def config4(width=2000, height=800) -> SceneSpec:
     return SceneSpec("config4", objs, cam, [light], shadows=True)
 
 
+CONFIG5_FPS = 12.0                   # scene-file time of frame f is f / CONFIG5_FPS seconds
+
+
+def config5_angle(frame: float, k: int, n_frames: int = 60) -> float:
+    """Rotation of object k about y at frame f: 2 pi f/60 (1 + k/8)."""
+    return 2 * math.pi * frame / n_frames * (1 + k / 8)
+
+
+def config5_light(frame: int, n_frames: int = 60) -> LightSpec:
+    """The point light on a radius-4 circle at y = 6 (scene files have no light
+    animation, scene.py:274-290, so the harness sets it per frame)."""
+    la = 2 * math.pi * frame / n_frames
+    return LightSpec("point", (4.0 * math.cos(la), 6.0, 4.0 * math.sin(la)), 0.4)
+
+
+def config5_keyframes(n_frames: int = 60, every: int = 10) -> dict:
+    """Object id -> [(time, R)] keyframes of the config-5 spin (a key every
+    `every` frames: at most 0.625 pi of rotation between keys, so slerp follows
+    the constant-rate spin about y)."""
+    base = config4()
+    return {o.id: [(f / CONFIG5_FPS, rotation_y(config5_angle(f, k, n_frames)) @ o.R)
+                   for f in range(0, n_frames + 1, every)]
+            for k, o in enumerate(base.objects)}
+
+
 def config5_frame(frame: int, n_frames: int = 60, width=2000, height=800) -> SceneSpec:
     """Dynamic scene: config 4 with object k rotating about y by
     2 pi f/60 (1 + k/8) and the light on a radius-4 circle at y = 6."""
     base = config4(width, height)
     objs = []
     for k, o in enumerate(base.objects):
-        ang = 2 * math.pi * frame / n_frames * (1 + k / 8)
-        objs.append(ObjSpec(o.id, o.kind, o.seed, rotation_y(ang) @ o.R, o.T, o.s))
-    la = 2 * math.pi * frame / n_frames
-    light = LightSpec("point", (4.0 * math.cos(la), 6.0, 4.0 * math.sin(la)), 0.4)
-    return SceneSpec(f"config5[{frame}]", objs, base.camera, [light], shadows=True)
+        objs.append(ObjSpec(o.id, o.kind, o.seed, rotation_y(config5_angle(frame, k, n_frames)) @ o.R, o.T, o.s))
+    return SceneSpec(f"config5[{frame}]", objs, base.camera, [config5_light(frame, n_frames)], shadows=True)
 
 
 def sweep_rays(n: int, box_min, box_max, seed: int = 0):

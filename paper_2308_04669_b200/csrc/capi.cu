@@ -279,6 +279,7 @@ int prepare_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject* obj
   int rc = check_camera(cam);
   if (rc) return rc;
   if (!fb) return fail(NEDF_ERR_INVALID, "frame buffers are NULL");
+  CUDA_TRY(cudaSetDevice(ctx->device));
   rc = build_scene(ctx, objs, n_objs, fields, n_fields, F.sc, st);
   if (rc) return rc;
   for (int s = 0; s < n_objs; ++s) {
@@ -407,7 +408,6 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
     int ctas = ctx->tc_ctas > 0 ? ctx->tc_ctas : ctx->n_sms;
     if ((rc = prof_mark(ctx, st, 0, true))) return rc;
     switch (ctx->tc_kernel) {
-      case NEDF_TC_PAIR: LAUNCH(ctx, launch_mlp_tc2(a, ctas, st)); break;
       case NEDF_TC_SINGLE: LAUNCH(ctx, launch_mlp_tc(a, ctas, 1, st)); break;
       case NEDF_TC_MCAST4: LAUNCH(ctx, launch_mlp_tc(a, ctas, 4, st)); break;
       default: LAUNCH(ctx, launch_mlp_tc(a, ctas, 2, st)); break;
@@ -590,7 +590,7 @@ int nedf_set_option(NedfContext* c, int key, int64_t v) {
       c->profile = v != 0;
       return NEDF_OK;
     case NEDF_OPT_TC_KERNEL:
-      if (v < NEDF_TC_AUTO || v > NEDF_TC_MCAST4) return fail(NEDF_ERR_INVALID, "bad tensor-core kernel");
+      if (v < NEDF_TC_AUTO || v > NEDF_TC_MCAST4 || v == 2) return fail(NEDF_ERR_INVALID, "bad tensor-core kernel");
       c->tc_kernel = (int)v;
       return NEDF_OK;
     case NEDF_OPT_GUARD_CLUSTER:
@@ -618,6 +618,7 @@ int nedf_stats_snapshot(NedfContext* c, int slot, NedfStepStats* out, void* stre
   if (!c || !out) return fail(NEDF_ERR_INVALID, "NULL argument");
   if (slot < 0 || slot >= kStatSlots) return fail(NEDF_ERR_INVALID, "stats slot out of range");
   memset(out, 0, sizeof(*out));
+  CUDA_TRY(cudaSetDevice(c->device));
   if (c->stats.ptr) {
     CUDA_TRY(launch_stats_export(c->stats.as<unsigned long long>(), c->stats_host_dev + 8 * slot,
                                  (cudaStream_t)stream));
@@ -645,6 +646,7 @@ int nedf_stats_slot(NedfContext* c, int slot, NedfStepStats* out) {
 int nedf_read_stats(NedfContext* c, NedfStepStats* out, void* stream) {
   if (!c || !out) return fail(NEDF_ERR_INVALID, "NULL argument");
   unsigned long long h[8] = {0};
+  CUDA_TRY(cudaSetDevice(c->device));
   if (c->stats.ptr) {
     cudaStream_t st = (cudaStream_t)stream;
     CUDA_TRY(launch_stats_export(c->stats.as<unsigned long long>(), c->stats_host_dev + 8 * kStatSlots, st));
@@ -675,6 +677,17 @@ int nedf_read_stats(NedfContext* c, NedfStepStats* out, void* stream) {
   c->ev_pairs.clear();
   c->ev_used = 0;
   return NEDF_OK;
+}
+
+// Logit z* at which the reference's alpha decision sigmoid(z) > thr (nn.py:169-175,
+// model.py:292, float64) changes; the tensor-core kernel re-evaluates rays whose
+// alpha logit lies within the fp16 error of z*.  thr = 0: sigmoid(z) is exactly 0 only
+// once exp(z) underflows (z < -745.13); thr < 0, thr >= 1 or NaN: the decision is the
+// same for every finite z, so there is nothing to guard (+inf never passes the test).
+static float alpha_boundary_logit(double thr) {
+  if (!(thr > 0.0)) return thr == 0.0 ? -745.1332f : INFINITY;
+  if (thr >= 1.0) return INFINITY;
+  return (float)(log(thr) - log1p(-thr));
 }
 
 int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* params, size_t n_params,
@@ -723,6 +736,7 @@ int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* 
     h.h[a] = hh > 0.0 ? hh : 1.0;
   }
   h.alpha_threshold = (double)info->alpha_threshold;
+  h.alpha_zthr = alpha_boundary_logit(h.alpha_threshold);
   h.n_layers = nl;
   for (int l = 0; l < nl; ++l) { h.wT_off[l] = wt_off[l]; h.b_off[l] = b_off[l]; }
   auto cleanup = [&]() {
@@ -745,7 +759,11 @@ int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* 
   h.bias = m->bias;
   // tensor-core operand image (paper-shaped models)
   h.tensor_ok = 0;
-  if (tc_available() && F == 256 && info->n_coarse + 1 + info->n_fine <= 256) {
+  // exactly the paper profile (nn.py:59-112 with PROFILES["paper"], model.py:35): the packers
+  // below lay out 16 head points x 63 features, 32 body layers of 256 and a 128 + 65 tail;
+  // any other shape runs on the fp32 path (mlp_simt.cu)
+  if (tc_available() && F == 256 && info->d_in == kDin && info->n_blocks == 16 && info->n_coarse == 64 &&
+      info->n_fine == 128) {
     size_t bytes = 0;
     e = tc_pack_weights(params, info->d_in, F, info->n_blocks, info->n_coarse, info->n_fine, &m->wpack,
                         &m->bias_pack, &bytes);
@@ -824,6 +842,7 @@ int nedf_model_tensor_ok(const NedfModel* m) { return m && m->host.tensor_ok ? 1
 static int single_model_frame(NedfContext* ctx, const NedfModel* m, int64_t n, Frame& F, cudaStream_t st) {
   if (!ctx || !m) return fail(NEDF_ERR_INVALID, "NULL argument");
   if (n < 0 || n > 0xFFFFFFFFll) return fail(NEDF_ERR_INVALID, "bad batch size");
+  CUDA_TRY(cudaSetDevice(ctx->device));
   F.sc.group_models.assign(1, m);
   F.sc.objs_per_group.assign(1, 1);
   F.sc.all_tc = m->host.tensor_ok != 0;
@@ -1001,6 +1020,7 @@ int nedf_composite(NedfContext* ctx, NedfFrameBuffers* fb, int width, void* stre
   if (!ctx || !fb) return fail(NEDF_ERR_INVALID, "NULL argument");
   int64_t n = (int64_t)fb->n_rows * width;
   if (n <= 0 || !fb->image_dev) return NEDF_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
   LAUNCH(ctx, launch_composite(fb->rgb_dev, fb->shadow_dev, fb->image_dev, n, ctx->n_sms, (cudaStream_t)stream));
   return NEDF_OK;
 }

@@ -31,6 +31,8 @@ struct DevModel {
   double bmin[3], bmax[3];       // relaxed sampling box
   double c[3], h[3];             // box centre and half extents (h==0 -> 1)
   double alpha_threshold;
+  float alpha_zthr;              // logit where sigmoid(z) > alpha_threshold flips (+-inf: never flips)
+  int pad_;
   const float* wT;               // fp32 [in][out] per layer (head padded to 1024 rows)
   const float* bias;             // fp32 per layer, concatenated
   const __half* wpack;           // tcgen05 operand image (see mlp_tc.cu)

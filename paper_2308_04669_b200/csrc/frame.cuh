@@ -5,6 +5,15 @@
 
 namespace nedf {
 
+// One-time kernel setup (attributes, occupancy queries) is cached per device: one
+// process may drive several GPUs, each through its own context.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d >= 0 && d < kMaxDevices ? d : 0;
+}
+
 struct FrameJob {
   RayJob ray;                    // camera / light / object tables
   const NedfField* fields;       // device copy of the field nodes
@@ -74,7 +83,6 @@ bool tc_available();
 // csize = CTAs per cluster sharing one multicast weight stream (1, 2 or 4)
 cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, int csize, cudaStream_t stream);
 // CTA-pair variant (mlp_tc2.cu): same contract, 256-ray tiles on SM pairs; n_ctas is rounded down to even
-cudaError_t launch_mlp_tc2(const TcArgs& a, int n_ctas, cudaStream_t stream);
 cudaError_t tc_pack_weights(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
                             __half** wpack_dev, float** bias_dev, size_t* bytes);
 

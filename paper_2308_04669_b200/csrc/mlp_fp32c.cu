@@ -411,7 +411,8 @@ namespace nedf {
 template <int KC>
 cudaError_t launch_guard(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out, int n_sms,
                          cudaStream_t stream) {
-  static int max_clusters = 0;
+  static int max_clusters_dev[kMaxDevices] = {};
+  int& max_clusters = max_clusters_dev[current_device()];
   const size_t smem = sizeof(ClSmem<KC>);
   if (max_clusters == 0) {
     cudaError_t e = cudaFuncSetAttribute(mlp_fp32_cluster_kernel<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -244,7 +244,8 @@ mlp_fp32_stream_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
 template <int R>
 static cudaError_t launch_stream(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
                                  int n_sms, cudaStream_t stream) {
-  static bool configured = false;
+  static bool configured_dev[kMaxDevices] = {};
+  bool& configured = configured_dev[current_device()];
   const size_t smem = sizeof(StreamSmem<R>);
   static_assert(sizeof(StreamSmem<R>) <= 227 * 1024, "shared memory budget");
   if (!configured) {

@@ -14,6 +14,7 @@
 // read transposed [in][out] so a warp's weight loads are coalesced.
 #include "common.cuh"
 #include "encode.cuh"
+#include "frame.cuh"
 
 namespace nedf {
 
@@ -263,7 +264,8 @@ size_t simt_smem_bytes() { return sizeof(SimtSmem); }
 
 cudaError_t launch_mlp_fp32(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
                             int n_sms, cudaStream_t stream) {
-  static bool configured = false;
+  static bool configured_dev[kMaxDevices] = {};
+  bool& configured = configured_dev[current_device()];
   size_t smem = sizeof(SimtSmem);
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(mlp_fp32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

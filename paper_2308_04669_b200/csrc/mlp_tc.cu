@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
         const float thr = a.guard * S_;
         const uint32_t pix = ls.pix[base + row], obj = ls.obj[base + row];
         const bool risky =
-            a.use_guard && (!(S_ < INFINITY) || (fb - fs) < thr || (cbest - csecond) < thr || fabsf(al) < thr);
+            a.use_guard && (!(S_ < INFINITY) || (fb - fs) < thr || (cbest - csecond) < thr || fabsf(al - m.alpha_zthr) < thr);
         if (a.out.mode == OUT_LOGITS) {
           // diagnostics: logits already written
         } else if (risky) {
@@ -684,8 +684,11 @@ extern "C" int nedf_diag_tc_trace(int enable, unsigned long long* out, int n) {
 namespace nedf {
 
 cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, int csize, cudaStream_t stream) {
-  static bool configured = false;
-  static int max_clusters[5] = {0, 0, 0, 0, 0};
+  static bool configured_dev[kMaxDevices] = {};
+  static int max_clusters_dev[kMaxDevices][5] = {};
+  const int dev = current_device();
+  bool& configured = configured_dev[dev];
+  int* max_clusters = max_clusters_dev[dev];
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(nedf_mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kSmemBytes);

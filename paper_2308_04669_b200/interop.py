@@ -89,12 +89,12 @@ def scene_from_reference(scene, device=None) -> list:
     for inst in scene:
         be = inst.depth
         bname = type(be).__name__
-        if bname == "NedfDepthBackend":
+        if isinstance(be, (NedfDepthBackend, OracleDepthBackend)):
+            depth = be                                   # already this package's (e.g. scene.load_scene)
+        elif bname == "NedfDepthBackend":
             depth = NedfDepthBackend(model_from_reference(be.model, device))
         elif bname == "OracleDepthBackend":
             depth = OracleDepthBackend(field_from_reference(be.oracle))
-        elif isinstance(be, (NedfDepthBackend, OracleDepthBackend)):
-            depth = be
         else:
             raise TypeError(f"unsupported depth backend {bname}")
         out.append(SceneInstance(int(inst.id), _transform(inst.transform), depth, field_from_reference(inst.radiance)))

@@ -422,7 +422,7 @@ class _LazyTiming(dict):
     host-side entries (kernel_launches, h2d_bytes) are there at once; the first
     access to anything else waits for the frame's last event and fills in the
     step times and the device counters (from a mapped stats slot, valid for the
-    next 63 frames).  Behaves as a plain dict afterwards."""
+    next 62 frames).  Behaves as a plain dict afterwards."""
 
     _EAGER = ("kernel_launches", "h2d_bytes")
 
@@ -496,7 +496,7 @@ def compose_frame(scene, camera: Camera, lights, config: RenderConfig | None = N
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     ctx = _ctx(buffers)
     st = _lib.stream_handle()
-    ctx.snapshot_stats(st)                 # reset the per-frame counters (no sync)
+    ctx.reset_stats(st)                    # zero the per-frame counters (no sync)
     ev[0].record()
     if changed_ids is None:
         nedf_generation_step(scene, camera, buffers, _tables=tb)

@@ -13,10 +13,3 @@ for ts in (0, 1):
             e0.record(); f(ts, N, 4096, pc, out.data_ptr()); e1.record(); torch.cuda.synchronize()
             cyc = out.item() / 4096
             print(f"{'TS' if ts else 'SS'} N={N:3d} variant={'warp-uniform-elect' if pc==-2 else 'single-thread-unrolled'}: {cyc:7.1f} cycles/MMA (ideal {128*N/256:.0f}); kernel {e0.elapsed_time(e1)*1e3:.1f} us")
-g = lib.nedf_diag_mma2_rate
-g.restype = C.c_int; g.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p]
-for ts in (0, 1):
-    for N in (64, 128, 256):
-        g(ts, N, 4096, out.data_ptr()); torch.cuda.synchronize()
-        g(ts, N, 4096, out.data_ptr()); torch.cuda.synchronize()
-        print(f"PAIR {'TS' if ts else 'SS'} N={N:3d}: {out.item() / 4096:7.1f} cycles/MMA (M=256; ideal per SM {128*N/256:.0f})")

@@ -182,6 +182,166 @@ def gen_frames():
          image=res.image)
 
 
+def _frame_compact(res, scene):
+    """A full-size frame stored compactly: depth f32 at covered pixels, id int16,
+    image u16 (quantised to 1/65535: PSNR contribution > 100 dB), and per pixel the
+    second-nearest object plane (f32 depth, id) so a GPU id mismatch can be checked
+    against the north star's "two surfaces within tolerance" rule."""
+    b = res.buffers
+    H, W = b.id.shape
+    planes = np.stack([b.per_object_depth[i.id] for i in scene]).reshape(len(scene), -1)
+    ids = np.array([i.id for i in scene])
+    order = np.argsort(planes, axis=0, kind="stable")
+    second = order[1] if len(scene) > 1 else np.zeros(H * W, dtype=np.int64)
+    d2 = planes[second, np.arange(H * W)]
+    id2 = np.where(np.isfinite(d2), ids[second], -1)
+    return dict(depth=b.depth.astype(np.float32), id=b.id.astype(np.int16),
+                image_u16=np.round(np.clip(res.image, 0, 1) * 65535).astype(np.uint16),
+                shadow_u8=np.round(b.shadow * 250).astype(np.uint8),
+                second_depth=np.where(np.isfinite(d2), d2, np.inf).astype(np.float32).reshape(H, W),
+                second_id=id2.astype(np.int16).reshape(H, W), scene_ids=ids)
+
+
+def gen_fullsize():
+    """The bench workload itself: config 4 at 2000x800 through the reference's
+    compose_frame (about 4 min on 8 cores), stored compactly (_frame_compact)."""
+    import time
+    spec = cfgs.config4()
+    scene, cam, lights, cfg = ref_scene(spec)
+    t = time.time()
+    res = pipeline.compose_frame(scene, cam, lights, cfg)
+    print(f"config4 2000x800 reference frame: {time.time() - t:.1f} s")
+    save("frame_config4_2000x800.npz", **_frame_compact(res, scene))
+
+
+def _scene_models():
+    """scenes/models/*.nedm (the random-init files the scene JSONs name), written
+    from the reference's own new_model + save_nedf bytes."""
+    d = ROOT / "scenes" / "models"
+    d.mkdir(parents=True, exist_ok=True)
+    for kind, seed in (("sphere", 0), ("box", 1), ("torus", 5)):
+        p = d / f"{kind}_seed{seed}.nedm"
+        if not p.exists():
+            p.write_bytes(paper_model(seed, kind)[1])
+
+
+def _ref_frame_from_desc(desc, time=None, width=None, height=None, lights=None):
+    from nedf import scene as rscene  # noqa: F401
+    if width is not None:
+        desc.camera_spec["width"], desc.camera_spec["height"] = width, height
+    inst = desc.instantiate(time)
+    res = pipeline.compose_frame(inst, desc.camera(), lights if lights is not None else desc.build_lights(),
+                                 desc.render_config())
+    return inst, res
+
+
+def gen_scenes():
+    """Scene files through the reference's load_scene (scene.py:310-366) and
+    evaluate_animation (scene.py:128-144): poses of the config-5 keyframe tracks,
+    the canonical dump, and frames of config 5 rendered from the JSON."""
+    from nedf import scene as rscene
+    _scene_models()
+    desc = rscene.load_scene(ROOT / "scenes" / "config5.json")
+    times = np.concatenate([np.linspace(-0.5, 5.5, 25), np.array([7, 38]) / 12.0])
+    R = np.zeros((len(times), len(desc.objects), 3, 3))
+    T = np.zeros((len(times), len(desc.objects), 3))
+    S = np.zeros((len(times), len(desc.objects)))
+    for i, t in enumerate(times):
+        for j, spec in enumerate(desc.objects):
+            g = rscene.evaluate_animation(spec.animation, float(t))
+            R[i, j], T[i, j], S[i, j] = g.rotation, g.translation, g.scale
+    dump = rscene.dumps_scene(desc)
+    save("scene_poses.npz", times=times, R=R, T=T, s=S,
+         dump=np.frombuffer(dump.encode(), dtype=np.uint8))
+    for f in (7, 38):
+        d = rscene.load_scene(ROOT / "scenes" / "config5.json")
+        L = cfgs.config5_light(f)
+        inst, res = _ref_frame_from_desc(d, time=f / 12.0, width=100, height=40,
+                                         lights=[pipeline.PointLight(np.asarray(L.vec, dtype=np.float64), L.beta)])
+        b = res.buffers
+        save(f"frame_config5json_f{f}_100x40.npz", depth=b.depth, id=b.id, rgb=b.rgb, shadow=b.shadow,
+             image=res.image, planes=np.stack([b.per_object_depth[i.id] for i in inst]))
+
+
+def gen_trained():
+    """Config-4 placements with the GPU-distilled paper-profile fixtures
+    (tests/golden/trained_*.nedm, scripts/distill_fixtures.py) through the
+    reference's load_scene + compose_frame: at 1000x400 with the stored alpha
+    threshold (0.5), and at 400x160 with the same weights under an alpha
+    threshold of 0.625 (model.py:354-369)."""
+    import shutil
+    import struct
+    import time
+    from nedf import scene as rscene
+    src = ROOT / "scenes" / "config4_trained.json"
+    t = time.time()
+    desc = rscene.load_scene(src)
+    inst, res = _ref_frame_from_desc(desc, width=1000, height=400)
+    print(f"trained config4 1000x400: {time.time() - t:.1f} s")
+    save("frame_trained_1000x400.npz", **_frame_compact(res, inst))
+    with tempfile.TemporaryDirectory() as td:
+        td = Path(td)
+        (td / "scenes").mkdir()
+        (td / "tests" / "golden").mkdir(parents=True)
+        for kind in ("sphere", "box", "torus"):
+            raw = (HERE / f"trained_{kind}.nedm").read_bytes()
+            (td / "tests" / "golden" / f"trained_{kind}.nedm").write_bytes(raw[:-4] + struct.pack("<f", 0.625))
+        shutil.copy(src, td / "scenes" / src.name)
+        desc = rscene.load_scene(td / "scenes" / src.name)
+        assert all(abs(desc.shared_model(o.nedf_model).alpha_threshold - 0.625) < 1e-9 for o in desc.objects)
+        inst, res = _ref_frame_from_desc(desc, width=400, height=160)
+        b = res.buffers
+        save("frame_trained_a0625_400x160.npz", depth=b.depth, id=b.id, rgb=b.rgb, shadow=b.shadow,
+             image=res.image, planes=np.stack([b.per_object_depth[i.id] for i in inst]))
+
+
+def gen_hazard():
+    """Slab-clip hazards (geometry.py:258-280) through the
+    reference's query_rays (model.py:277-293) on the trained sphere fixture (relaxed
+    box [-1.5, 1.5]^3): rays on slab planes parallel to an axis (0 * inf = NaN ->
+    widened slab), along box edges, grazing an edge / corner (t_exit == t_enter, 16
+    identical sample points), signed-zero directions, origins inside the box, boxes
+    behind the origin, plus the random rays of geometry.npz."""
+    m = model.load_nedf(HERE / "trained_sphere.nedm")
+    box = m.relaxed_box
+    b = 1.5
+    r2 = 1.0 / np.sqrt(2.0)
+    rows = [
+        ((-b, 0.0, -3.0), (0.0, 0.0, 1.0)),          # on the x = min plane, parallel to it
+        ((b, 0.0, -3.0), (0.0, 0.0, 1.0)),           # on the x = max plane
+        ((b, b, -3.0), (0.0, 0.0, 1.0)),             # along an edge
+        ((-b, -b, -3.0), (0.0, 0.0, 1.0)),
+        ((0.0, b, -3.0), (0.0, 0.0, 1.0)),
+        ((2.0, 0.0, -3.0), (0.0, 0.0, 1.0)),         # parallel, outside the slab: miss
+        ((0.0, -3.0, 0.0), (r2, r2, 0.0)),           # grazes the edge x = b, y = -b (t0 == t1 up to rounding)
+        ((0.0, 0.0, -3.0), (0.0, 0.0, 1.0)),         # straight through the centre
+        ((0.0, 0.0, 0.0), (0.0, 0.0, 1.0)),          # origin at the centre: t0 clamps to 0
+        ((0.3, -0.2, 1.4), (0.1, 0.2, -0.9)),        # origin inside
+        ((0.0, 0.0, 3.0), (0.0, 0.0, 1.0)),          # box behind the origin: miss
+        ((-0.0, 0.0, -3.0), (-0.0, -0.0, 1.0)),      # signed zeros
+        ((-3.0, -3.0, -3.0), (1.0, 1.0, 1.0)),       # through two corners
+        ((-3.0, b, b), (1.0, 0.0, 0.0)),             # along the edge y = z = max
+        ((b + 1e-12, 0.0, -3.0), (0.0, 0.0, 1.0)),   # just outside a plane: miss
+        ((b - 1e-12, 0.0, -3.0), (0.0, 0.0, 1.0)),   # just inside
+    ]
+    o = np.array([r[0] for r in rows], dtype=np.float64)
+    d = np.array([r[1] for r in rows], dtype=np.float64)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    # corner graze: from outside, aimed exactly at the corner (b, b, b) along a direction that only touches it
+    oc = np.array([[b + 1.0, b + 1.0, b - 1.0]])
+    dc = np.array([[-1.0, -1.0, 1.0]]) / np.sqrt(3.0)
+    g = np.load(HERE / "geometry.npz")
+    o = np.concatenate([o, oc, g["origins"]])
+    d = np.concatenate([d, dc, g["dirs"]])
+    t0, t1, hit = geometry.clip_rays_to_aabb(o, d, box)
+    mu, alpha = model.query_rays(m, o, d)
+    feats, h2 = geometry.sample_and_encode_rays(o, d, box)
+    assert np.array_equal(hit, h2)
+    lc, lf, la, _ = nn.forward(m.mlp, feats[hit])
+    save("hazard_rays.npz", origins=o, dirs=d, t0=t0, t1=t1, hit=hit, mu=mu, alpha=alpha,
+         logits_c=lc, logits_f=lf, logit_a=la[:, 0], n_special=len(rows) + 1)
+
+
 def gen_dynamic():
     # config 5 (dynamic scene): two frames of the 60-frame sequence -- objects rotated by different
     # amounts about y and the point light elsewhere on its orbit -- at 1/400 of the pixels

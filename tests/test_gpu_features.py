@@ -143,19 +143,59 @@ def test_zero_weights_decode_to_lowest_bins(P):
     _lib.context().set_option(_lib.OPT_PRECISION, _lib.PREC_AUTO)
 
 
-def test_full_size_config4_subsample_parity(P):
-    """The bench workload itself (2000x800, 8 objects, shadows) against the
-    float64 oracle on 4000 random pixels."""
+def compact_parity(b, image, g):
+    """frame_parity against a compact full-size golden (make_golden._frame_compact):
+    an id mismatch is allowed only where the GPU picked the reference's
+    second-nearest object and the two planes lie within the depth tolerance."""
+    from tests.parity import DEPTH_TOL, ID_FRACTION, PSNR_MIN
+    depth, ids = b["depth"], b["id"]
+    ref_id = g["id"].astype(np.int32)
+    rep, bad = {}, []
+    same = ids == ref_id
+    rep["pixels"] = int(ids.size)
+    rep["id_match"] = float(same.mean())
+    if rep["id_match"] < ID_FRACTION:
+        bad.append(f"id match {rep['id_match']:.6f}")
+    mism = ~same
+    rep["id_mismatch"] = int(mism.sum())
+    if mism.any():
+        ok = (ids[mism] == g["second_id"][mism]) & (np.abs(g["second_depth"][mism].astype(np.float64)
+                                                            - g["depth"][mism].astype(np.float64)) <= DEPTH_TOL)
+        if not ok.all():
+            bad.append(f"{int((~ok).sum())} id mismatches not between surfaces within tolerance")
+    both = same & (ref_id >= 0)
+    err = np.abs(depth[both] - g["depth"][both].astype(np.float64))
+    rep["depth_max_err"] = float(err.max())
+    over = err > DEPTH_TOL + 1e-6 * np.abs(depth[both])     # + f32 storage
+    rep["depth_n_over"] = int(over.sum())
+    rep["depth_over_pixels"] = np.flatnonzero(both.ravel())[over].tolist()[:50]
+    if rep["depth_n_over"]:
+        bad.append(f"depth err > tol on {rep['depth_n_over']} px")
+    if not np.isinf(depth[same & (ref_id < 0)]).all():
+        bad.append("missed pixels must have depth +inf")
+    ref_img = g["image_u16"].astype(np.float64) / 65535.0
+    rep["psnr"] = psnr(image, ref_img)
+    if rep["psnr"] < PSNR_MIN:
+        bad.append(f"PSNR {rep['psnr']:.2f}")
+    if b.get("shadow") is not None:
+        rep["shadow_mismatch"] = int((np.round(b["shadow"] * 250).astype(np.uint8) != g["shadow_u8"]).sum())
+    return rep, bad
+
+
+def test_full_size_config4_matches_reference(P, golden):
+    """The bench workload itself (2000x800, 8 objects, point-light shadows): all
+    1.6M pixels against the REAL reference's compose_frame output
+    (tests/golden/frame_config4_2000x800.npz, make_golden.py gen_fullsize)."""
     _lib, fields, geometry, model, pipeline, scenes = _mods()
+    g = golden("frame_config4_2000x800.npz")
     spec = CF.config4()
     scene, cam, lights, cfg = scenes.build(spec)
     res = pipeline.compose_frame(scene, cam, lights, cfg)
     b = res.buffers.numpy()
-    img = res.image.cpu().numpy().reshape(-1, 3)
-    pix = np.random.default_rng(7).choice(cam.width * cam.height, size=4000, replace=False)
-    objs, ocam, olights, ocfg = oracle_scene(spec)
-    ref = O.render(objs, ocam, olights, ocfg, pixels=pix, threads=8)
-    rep, bad = frame_parity(b["depth"].ravel()[pix], b["id"].ravel()[pix], img[pix], ref.depth, ref.id, ref.image)
+    rep, bad = compact_parity(b, res.image.cpu().numpy(), g)
+    rep["guarded_evals"] = res.timing["guarded_evals"]
+    rep["network_evals"] = res.timing["network_evals"]
+    print("config4 2000x800 vs reference:", rep)
     assert not bad, (rep, bad)
     assert res.timing["network_evals"] > 1_000_000
 
@@ -224,36 +264,29 @@ def test_precision_modes_agree_on_decisions(P):
 
 @pytest.mark.parametrize("prec", ["auto", "tensor"])
 def test_tensor_kernel_variants_agree(P, prec):
-    """Single-CTA, CTA-pair (M = 256, cta_group::2) and cluster-multicast
-    kernels run the same fp16 x fp16 -> fp32 chain; with the guard all must
-    reach the same decisions."""
+    """Single-CTA and cluster-multicast kernels run the same fp16 x fp16 -> fp32
+    chain per CTA: bit-identical decisions with or without the guard."""
     _lib, fields, geometry, model, pipeline, scenes = _mods()
     ctx = _lib.context()
     ctx.set_option(_lib.OPT_PRECISION, {"auto": _lib.PREC_AUTO, "tensor": _lib.PREC_TENSOR}[prec])
     scene, cam, lights, cfg = scenes.build(CF.config4(300, 120))
     out = {}
-    for name, k in (("single", _lib.TC_SINGLE), ("pair", _lib.TC_PAIR), ("mcast2", _lib.TC_MCAST2),
-                    ("mcast4", _lib.TC_MCAST4)):
+    for name, k in (("single", _lib.TC_SINGLE), ("mcast2", _lib.TC_MCAST2), ("mcast4", _lib.TC_MCAST4)):
         ctx.set_option(_lib.OPT_TC_KERNEL, k)
         r = pipeline.compose_frame(scene, cam, lights, cfg)
         out[name] = r.buffers.numpy()
     ctx.set_option(_lib.OPT_TC_KERNEL, _lib.TC_AUTO)
     ctx.set_option(_lib.OPT_PRECISION, _lib.PREC_AUTO)
     a = out["single"]
-    for name in ("pair", "mcast2", "mcast4"):
+    for name in ("mcast2", "mcast4"):
         b = out[name]
-        same = a["id"] == b["id"]
-        if prec == "auto" or name != "pair":
-            # the multicast kernels run the identical per-CTA MMA sequence: bit-identical
-            assert same.all(), name
-            fin = np.isfinite(a["depth"])
-            np.testing.assert_allclose(a["depth"][fin], b["depth"][fin], rtol=0, atol=1e-9)
-        else:
-            assert same.mean() > 0.999
+        assert (a["id"] == b["id"]).all(), name
+        fin = np.isfinite(a["depth"])
+        np.testing.assert_allclose(a["depth"][fin], b["depth"][fin], rtol=0, atol=1e-9)
 
 
 def test_cluster_kernels_ragged_group_tails(P):
-    """Group sizes that leave later CTAs of a pair / cluster with 0, 1 or 127 rays."""
+    """Group sizes that leave later CTAs of a cluster with 0, 1 or 127 rays."""
     _lib, fields, geometry, model, pipeline, scenes = _mods()
     ctx = _lib.context()
     m = scenes.paper_model(0, "sphere")
@@ -263,7 +296,7 @@ def test_cluster_kernels_ragged_group_tails(P):
         d = np.tile([0.0, 0.0, 1.0], (n, 1)) + rng.normal(size=(n, 3)) * 0.05
         d /= np.linalg.norm(d, axis=1, keepdims=True)
         res = {}
-        kernels = (_lib.TC_SINGLE, _lib.TC_PAIR, _lib.TC_MCAST2, _lib.TC_MCAST4)
+        kernels = (_lib.TC_SINGLE, _lib.TC_MCAST2, _lib.TC_MCAST4)
         for k in kernels:
             ctx.set_option(_lib.OPT_TC_KERNEL, k)
             res[k] = model.query_rays(m, o, d)
@@ -283,22 +316,44 @@ def test_step_timing_report_shape(P):
 
 
 def test_image_tiles_match_full_frame(P):
-    """Multi-GPU partition on one GPU: each rank's stripes rendered with
-    FrameBuffers(rows=...) reassemble to the full frame bit-for-bit."""
+    """Multi-GPU partition on one GPU: each rank's interleaved rows rendered with
+    FrameBuffers(rows=...) reassemble to the full frame bit-for-bit, also through
+    the gather's device-side pack / unpack."""
+    import torch
     _lib, fields, geometry, model, pipeline, scenes = _mods()
     from paper_2308_04669_b200 import distributed as D
     scene, cam, lights, cfg = scenes.build(CF.config4(256, 96))
     full = pipeline.compose_frame(scene, cam, lights, cfg)
     ref_img = full.image.cpu().numpy()
     ref = full.buffers.numpy()
-    world = 3
-    img = np.zeros_like(ref_img)
-    ids = np.zeros_like(ref["id"])
-    for r in range(world):
-        rows = D.stripe_rows(cam.height, r, world)
+    for world in (3, 8):
+        img = np.zeros_like(ref_img)
+        ids = np.zeros_like(ref["id"])
+        tiles = []
+        for r in range(world):
+            rows = D.interleave_rows(cam.height, r, world)
+            buf = pipeline.FrameBuffers(cam.width, cam.height, rows=rows)
+            res = pipeline.compose_frame(scene, cam, lights, cfg, buffers=buf)
+            img[rows] = res.image.cpu().numpy()
+            ids[rows] = buf.id.cpu().numpy()
+            tiles.append({"image": buf.image, "depth": buf.depth, "id": buf.id})
+        np.testing.assert_array_equal(ids, ref["id"])
+        np.testing.assert_array_equal(img, ref_img)
+        # the gather's reassembly on the device (rank 0's side of gather_tiles)
+        mr = D.max_rows(cam.height, world)
+        packed = [D.pack_tile(t, mr) for t in tiles]
+        g = torch.stack([p for p, _ in packed])
+        out = D.unpack_gathered(g, packed[0][1], mr, cam.height, world)
+        np.testing.assert_array_equal(out["image"].cpu().numpy(), ref_img)
+        np.testing.assert_array_equal(out["id"].cpu().numpy(), ref["id"])
+        np.testing.assert_array_equal(out["depth"].cpu().numpy(), ref["depth"])
+    # a frame shorter than the rank count: some ranks own no rows
+    scene, cam, lights, cfg = scenes.build(CF.config4(64, 5))
+    full = pipeline.compose_frame(scene, cam, lights, cfg).image.cpu().numpy()
+    img = np.zeros_like(full)
+    for r in range(8):
+        rows = D.interleave_rows(cam.height, r, 8)
         buf = pipeline.FrameBuffers(cam.width, cam.height, rows=rows)
         res = pipeline.compose_frame(scene, cam, lights, cfg, buffers=buf)
         img[rows] = res.image.cpu().numpy()
-        ids[rows] = buf.id.cpu().numpy()
-    np.testing.assert_array_equal(ids, ref["id"])
-    np.testing.assert_array_equal(img, ref_img)
+    np.testing.assert_array_equal(img, full)

@@ -6,13 +6,14 @@ the CUDA path (CPU only)."""
 
 import hashlib
 import json
+from pathlib import Path
 
 import numpy as np
 import pytest
 
 from oracle import nedf_oracle as O
 from paper_2308_04669_b200 import configs as C
-from tests.conftest import GOLDEN
+from tests.conftest import GOLDEN, ROOT
 from tests.helpers import oracle_model, oracle_scene
 
 
@@ -179,3 +180,80 @@ def test_nedm_format_errors():
         O.parse_nedm(raw[:-1])
     with pytest.raises(ValueError):
         O.parse_nedm(raw[:20])
+
+
+@pytest.fixture(scope="module")
+def trained():
+    return {k: O.parse_nedm((GOLDEN / f"trained_{k}.nedm").read_bytes()) for k in ("sphere", "box", "torus")}
+
+
+def test_hazard_rays(golden, trained):
+    """Slab-clip hazards (NaN slabs, edges, grazing edge / corner, signed zeros,
+    inside origins) on the trained sphere: clip bit-equal, logits to 1e-9, decisions
+    equal to the reference's query_rays."""
+    z = golden("hazard_rays.npz")
+    m = trained["sphere"]
+    t0, t1, hit = O.slab_clip(z["origins"], z["dirs"], m.box_min, m.box_max)
+    np.testing.assert_array_equal(hit, z["hit"])
+    np.testing.assert_array_equal(t0[hit], z["t0"][hit])
+    np.testing.assert_array_equal(t1[hit], z["t1"][hit])
+    mu, alpha, h2, (lc, lf, la) = O.query_local(m, z["origins"], z["dirs"], return_logits=True)
+    np.testing.assert_array_equal(h2, z["hit"])
+    scale = np.abs(z["logits_f"]).max()
+    np.testing.assert_allclose(lf, z["logits_f"], rtol=0, atol=1e-9 * scale)
+    np.testing.assert_allclose(lc, z["logits_c"], rtol=0, atol=1e-9 * scale)
+    np.testing.assert_allclose(la, z["logit_a"], rtol=0, atol=1e-9 * scale)
+    np.testing.assert_array_equal(mu[hit], z["mu"][hit])
+    np.testing.assert_array_equal(alpha, z["alpha"])
+
+
+def _desc_objs(desc, models, time=None):
+    """Oracle objects for a scene.SceneDescription (scene file -> oracle)."""
+    from paper_2308_04669_b200 import scene as S
+    objs = []
+    for spec in desc.objects:
+        g = desc.pose(spec, time)
+        geo = spec.geometry
+        prim = {"sphere": lambda: ("sphere", tuple(geo["center"]), geo["radius"]),
+                "box": lambda: ("box", tuple(geo["center"]), tuple(geo["half_extents"])),
+                "torus": lambda: ("torus", tuple(geo["center"]), geo["major_r"], geo["minor_r"])}[geo["type"]]()
+        key = str((desc.base_dir / spec.nedf_model).resolve())
+        if key not in models:
+            models[key] = O.parse_nedm(Path(key).read_bytes())
+        objs.append(O.Obj(spec.id, np.asarray(g.rotation), np.asarray(g.translation), float(g.scale), prim,
+                          model=models[key]))
+    c = desc.camera()
+    cam = O.Cam(np.asarray(c.position), np.asarray(c.orientation), c.fov_y, c.width, c.height)
+    return objs, cam
+
+
+def test_trained_frame_pixels(golden):
+    """The oracle on the trained fixtures through scenes/config4_trained.json:
+    a pixel sample of the reference's 1000x400 frame."""
+    from paper_2308_04669_b200 import scene as S
+    g = golden("frame_trained_1000x400.npz")
+    desc = S.load_scene(ROOT / "scenes" / "config4_trained.json")
+    desc.camera_spec["width"], desc.camera_spec["height"] = 1000, 400
+    objs, cam = _desc_objs(desc, {})
+    lights = [O.Light("point", np.asarray(L["position"], dtype=np.float64), L["beta"]) for L in desc.lights]
+    pix = np.random.default_rng(1).choice(1000 * 400, size=1500, replace=False)
+    out = O.render(objs, cam, lights, O.Config(), pixels=pix, threads=8)
+    np.testing.assert_array_equal(out.id, g["id"].ravel()[pix])
+    fin = np.isfinite(out.depth)
+    np.testing.assert_allclose(out.depth[fin], g["depth"].ravel()[pix][fin], rtol=2e-7)
+    np.testing.assert_allclose(out.image, g["image_u16"].reshape(-1, 3)[pix] / 65535.0, atol=1e-5)
+
+
+@pytest.mark.parametrize("frame", [7, 38])
+def test_scene_file_config5_frames(golden, frame):
+    """config 5 posed by the keyframe tracks of scenes/config5.json (reference
+    load_scene + evaluate_animation) -- the oracle reproduces the frames."""
+    from paper_2308_04669_b200 import scene as S
+    S.ensure_random_init_models(ROOT / "scenes" / "models", [("sphere", 0), ("box", 1), ("torus", 5)])
+    z = golden(f"frame_config5json_f{frame}_100x40.npz")
+    desc = S.load_scene(ROOT / "scenes" / "config5.json")
+    desc.camera_spec["width"], desc.camera_spec["height"] = 100, 40
+    objs, cam = _desc_objs(desc, {}, time=frame / C.CONFIG5_FPS)
+    L = C.config5_light(frame)
+    out = O.render(objs, cam, [O.Light("point", np.asarray(L.vec, dtype=np.float64), L.beta)], O.Config(), threads=4)
+    _check_frame(out, z)
