@@ -64,7 +64,12 @@ enum {
   NEDF_OPT_TC_CTAS = 3,         /* persistent CTAs for the tensor-core kernel (0 = one per SM) */
   NEDF_OPT_PROFILE = 4,         /* 1 = time every network launch with CUDA events (read back by nedf_read_stats) */
   NEDF_OPT_TC_KERNEL = 5,       /* one of NEDF_TC_*: which tensor-core network kernel runs */
-  NEDF_OPT_GUARD_CLUSTER = 6    /* near-tie guard kernel's cluster size: 4, 8, or 0 = by frame size */
+  NEDF_OPT_GUARD_CLUSTER = 6,   /* near-tie guard kernel's cluster size: 4, 8, or 0 = by frame size */
+  NEDF_OPT_SETUP_EXACT = 7,     /* 1 = every work-list box test in float64 (default 0: certified fp32 test,
+                                   float64 only where its error bound cannot decide; same lists either way) */
+  NEDF_OPT_FUSE = 8             /* 1 (default) = nedf_render_frame fuses the per-pixel passes (STEP 1 resolve,
+                                   STEP 2, shadow fill, first light's STEP 3 setup; last light's resolve +
+                                   composite); 0 = one kernel per step, as the step entry points run */
 };
 
 /* Tensor-core network kernels (NEDF_OPT_TC_KERNEL). */
@@ -177,6 +182,7 @@ typedef struct {
   double net_ms;            /* summed device time of the main network kernel (tensor-core or fp32) */
   double guard_ms;          /* summed device time of the fp32 re-evaluation of guarded rays */
   int64_t h2d_bytes;        /* host->device bytes this library copied (per-call scene tables) */
+  int64_t exact_clips;      /* (ray, object) box tests the certified fp32 test left to float64 */
 } NedfStepStats;
 
 /* ---- library / context ---------------------------------------------------- */
@@ -252,6 +258,13 @@ int nedf_render_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject*
                       const NedfField* fields, int n_fields, const NedfLight* lights, int n_lights,
                       const NedfRenderConfig* cfg, NedfFrameBuffers* fb, void* stream);
 
+/* nedf_render_frame that also records events[0..3] (cudaEvent_t, may be NULL) on the
+ * stream at frame start, end of STEP 1's network, end of STEP 2 and frame end, for
+ * compose_frame's per-step timing.  With NEDF_OPT_FUSE the STEP 1 resolve and the first
+ * light's STEP 3 ray setup run inside the STEP 2 interval. */
+int nedf_render_frame_timed(NedfContext* ctx, const NedfCamera* cam, const NedfObject* objs, int n_objs,
+                            const NedfField* fields, int n_fields, const NedfLight* lights, int n_lights,
+                            const NedfRenderConfig* cfg, NedfFrameBuffers* fb, void* const* events, void* stream);
 /* ---- output formats (imgio.py): per-pixel conversions on the GPU, so
  * only 8/16-bit planes or the f32 depth plane are copied to the host for encoding ---- */
 /* (clip(x, 0, 1) * 255 + 0.5) -> uint8, truncating like numpy astype (imgio.py:23-24);

@@ -25,6 +25,7 @@ NEDF_ERR_NOMEM = -5
 
 PREC_AUTO, PREC_TENSOR, PREC_FP32 = 0, 1, 2
 OPT_PRECISION, OPT_GUARD_PPM, OPT_TC_CTAS, OPT_PROFILE, OPT_TC_KERNEL, OPT_GUARD_CLUSTER = 1, 2, 3, 4, 5, 6
+OPT_SETUP_EXACT, OPT_FUSE = 7, 8
 TC_AUTO, TC_SINGLE, TC_MCAST2, TC_MCAST4 = 0, 1, 3, 4
 
 FIELD_SPHERE, FIELD_BOX, FIELD_TORUS, FIELD_PLANE, FIELD_UNION, FIELD_TRANSFORMED, FIELD_VOXEL = range(1, 8)
@@ -72,7 +73,7 @@ class NedfFrameBuffers(C.Structure):
 class NedfStepStats(C.Structure):
     _fields_ = [("evals", C.c_int64), ("guarded", C.c_int64), ("covered", C.c_int64), ("resampled", C.c_int64),
                 ("launches", C.c_int64), ("net_launches", C.c_int64), ("net_ms", C.c_double),
-                ("guard_ms", C.c_double), ("h2d_bytes", C.c_int64)]
+                ("guard_ms", C.c_double), ("h2d_bytes", C.c_int64), ("exact_clips", C.c_int64)]
 
 
 P = C.c_void_p
@@ -125,6 +126,10 @@ PROTOTYPES = {
     "nedf_render_frame": (C.c_int, [P, C.POINTER(NedfCamera), C.POINTER(NedfObject), C.c_int,
                                     C.POINTER(NedfField), C.c_int, C.POINTER(NedfLight), C.c_int,
                                     C.POINTER(NedfRenderConfig), C.POINTER(NedfFrameBuffers), P]),
+    "nedf_render_frame_timed": (C.c_int, [P, C.POINTER(NedfCamera), C.POINTER(NedfObject), C.c_int,
+                                          C.POINTER(NedfField), C.c_int, C.POINTER(NedfLight), C.c_int,
+                                          C.POINTER(NedfRenderConfig), C.POINTER(NedfFrameBuffers),
+                                          C.POINTER(P), P]),
 }
 
 _lib = None
@@ -190,7 +195,7 @@ class Context:
         check(self._lib.nedf_read_stats(self.handle, C.byref(s), stream))
         return {"evals": s.evals, "guarded": s.guarded, "covered": s.covered, "resampled": s.resampled,
                 "launches": s.launches, "net_launches": s.net_launches, "net_ms": s.net_ms,
-                "guard_ms": s.guard_ms, "h2d_bytes": s.h2d_bytes}
+                "guard_ms": s.guard_ms, "h2d_bytes": s.h2d_bytes, "exact_clips": s.exact_clips}
 
     _RESET_SLOT = 63                     # mapped slot 63 only absorbs resets; 0-62 rotate
 
@@ -221,7 +226,8 @@ class Context:
                                f"{self._RESET_SLOT} steps")
         s = NedfStepStats()
         check(self._lib.nedf_stats_slot(self.handle, slot, C.byref(s)))
-        return {"evals": s.evals, "guarded": s.guarded, "covered": s.covered, "resampled": s.resampled}
+        return {"evals": s.evals, "guarded": s.guarded, "covered": s.covered, "resampled": s.resampled,
+                "exact_clips": s.exact_clips}
 
     def __del__(self):
         try:

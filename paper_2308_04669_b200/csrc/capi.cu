@@ -74,6 +74,8 @@ struct NedfContext {
   int tc_ctas = 0;
   int tc_kernel = NEDF_TC_AUTO;
   int guard_cluster = 0;
+  int setup_exact = 0;
+  int fuse = 1;
   int profile = 0;
   int64_t launches = 0;
   // event pairs around network launches (NEDF_OPT_PROFILE); kind 0 = main, 1 = guard
@@ -177,6 +179,13 @@ int build_scene(NedfContext* ctx, const NedfObject* objs, int n_objs, const Nedf
         for (int i = 0; i < 3; ++i)
           d.bs_c[i] = (float)(o.T[i] + o.s * (o.R[3 * i] * cl[0] + o.R[3 * i + 1] * cl[1] + o.R[3 * i + 2] * cl[2]));
         d.bs_r = (float)(o.s * std::sqrt(r2));
+        for (int i = 0; i < 9; ++i) d.Rf[i] = (float)o.R[i];
+        for (int i = 0; i < 3; ++i) {
+          d.Tf[i] = (float)o.T[i];
+          d.bminf[i] = (float)hm.bmin[i];
+          d.bmaxf[i] = (float)hm.bmax[i];
+        }
+        d.inv_sf = (float)(1.0 / o.s);
       }
       if (!o.model->host.tensor_ok) sc.all_tc = false;
     } else if (o.depth_kind == NEDF_DEPTH_ANALYTIC) {
@@ -439,12 +448,13 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
   return NEDF_OK;
 }
 
-int do_step1(NedfContext* ctx, Frame& F, cudaStream_t st) {
+// resolve = false: leave the z-keys for the fused resolve_shade_kernel
+int do_step1(NedfContext* ctx, Frame& F, cudaStream_t st, bool resolve = true) {
   FrameJob& fj = F.fj;
   fj.ray.mode = RAY_PRIMARY;
   CUDA_TRY(cudaMemsetAsync(F.ls.count, 0, 64 * sizeof(int), st));
   if (F.n_pix == 0) return NEDF_OK;
-  LAUNCH(ctx, launch_setup(fj, F.gt, F.ls, RAY_PRIMARY, ctx->n_sms, st));
+  LAUNCH(ctx, launch_setup(fj, F.gt, F.ls, RAY_PRIMARY, ctx->setup_exact, ctx->n_sms, st));
   OutSpec out;
   memset(&out, 0, sizeof(out));
   out.mode = OUT_ZBUF;
@@ -454,7 +464,7 @@ int do_step1(NedfContext* ctx, Frame& F, cudaStream_t st) {
   int rc = run_network(ctx, F, fj.ray, out, st);
   if (rc) return rc;
   if (fj.planes != nullptr) LAUNCH(ctx, launch_recombine(fj, ctx->n_sms, st));   // plane cache kept
-  else LAUNCH(ctx, launch_step1_resolve(fj, F.gt, ctx->n_sms, st));
+  else if (resolve) LAUNCH(ctx, launch_step1_resolve(fj, F.gt, ctx->n_sms, st));
   return NEDF_OK;
 }
 
@@ -492,37 +502,105 @@ double default_eps(const Frame& F, const NedfObject* objs) {
   return e;
 }
 
-int do_step3(NedfContext* ctx, Frame& F, const NedfObject* objs, const NedfLight* L, const NedfRenderConfig* cfg,
-             cudaStream_t st) {
+// STEP 3 job of one light: the frame job with the light's ray mode, epsilon
+// (pipeline.py:202-208 default) and beta; z-keys in the context's shadow keys.
+int make_shadow_job(NedfContext* ctx, const Frame& F, const NedfObject* objs, const NedfLight* L,
+                    const NedfRenderConfig* cfg, FrameJob& sj, int& mode) {
   if (!L) return fail(NEDF_ERR_INVALID, "light is NULL");
   if (!(L->beta > 0.0 && L->beta < 1.0)) return fail(NEDF_ERR_INVALID, "shadow intensity beta must be in (0, 1)");
-  int mode;
   if (L->kind == NEDF_LIGHT_POINT) mode = RAY_POINT_SHADOW;
   else if (L->kind == NEDF_LIGHT_DIRECTIONAL) mode = RAY_DIR_SHADOW;
   else return fail(NEDF_ERR_UNSUPPORTED, "unsupported light type");
-  FrameJob& fj = F.fj;
-  fill_config(fj, cfg);
+  sj = F.fj;
+  fill_config(sj, cfg);
   double eps = (cfg && cfg->shadow_epsilon > 0.0) ? cfg->shadow_epsilon : default_eps(F, objs);
-  fj.eps = eps;
-  fj.beta = L->beta;
-  fj.ray.mode = mode;
-  fj.ray.eps = eps;
-  fj.ray.depth64 = fj.depth;
-  for (int a = 0; a < 3; ++a) fj.ray.light[a] = L->vec[a];
-  CUDA_TRY(cudaMemsetAsync(F.ls.count, 0, 64 * sizeof(int), st));
-  if (F.n_pix == 0) return NEDF_OK;
-  FrameJob sj = fj;
+  sj.eps = eps;
+  sj.beta = L->beta;
+  sj.ray.mode = mode;
+  sj.ray.eps = eps;
+  sj.ray.depth64 = F.fj.depth;
+  for (int a = 0; a < 3; ++a) sj.ray.light[a] = L->vec[a];
   sj.planes = nullptr;
   sj.key = ctx->skey.as<unsigned long long>();
-  LAUNCH(ctx, launch_setup(sj, F.gt, F.ls, mode, ctx->n_sms, st));
+  return NEDF_OK;
+}
+
+// STEP 3 for one light.  lists_ready: the light's work lists and z-keys were
+// built by resolve_shade_kernel.  image != NULL: the resolve also composites.
+int do_step3(NedfContext* ctx, Frame& F, const NedfObject* objs, const NedfLight* L, const NedfRenderConfig* cfg,
+             cudaStream_t st, float* image = nullptr, bool lists_ready = false) {
+  FrameJob sj;
+  int mode = 0;
+  int rc = make_shadow_job(ctx, F, objs, L, cfg, sj, mode);
+  if (rc) return rc;
+  if (!lists_ready) {
+    CUDA_TRY(cudaMemsetAsync(F.ls.count, 0, 64 * sizeof(int), st));
+    if (F.n_pix == 0) return NEDF_OK;
+    LAUNCH(ctx, launch_setup(sj, F.gt, F.ls, mode, ctx->setup_exact, ctx->n_sms, st));
+  }
+  if (F.n_pix == 0) return NEDF_OK;
   OutSpec out;
   memset(&out, 0, sizeof(out));
   out.mode = OUT_ZBUF;
   out.key = sj.key;
-  int rc = run_network(ctx, F, sj.ray, out, st);
+  rc = run_network(ctx, F, sj.ray, out, st);
   if (rc) return rc;
-  LAUNCH(ctx, launch_shadow_resolve(sj, F.gt, mode, ctx->n_sms, st));
+  LAUNCH(ctx, launch_shadow_resolve(sj, F.gt, mode, image, ctx->n_sms, st));
   return NEDF_OK;
+}
+
+int record(void* const* events, int i, cudaStream_t st) {
+  if (events && events[i]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[i], st));
+  return NEDF_OK;
+}
+
+// compose_frame (pipeline.py:430-468) on the device.  Fused (ctx->fuse, no plane
+// cache): setup -> network -> [resolve + shade + shadow fill + light 0 setup] ->
+// per light: network -> resolve (+ composite for the last light).
+int render_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject* objs, int n_objs,
+                 const NedfField* fields, int n_fields, const NedfLight* lights, int n_lights,
+                 const NedfRenderConfig* cfg, NedfFrameBuffers* fb, void* const* events, cudaStream_t st) {
+  if (!ctx) return fail(NEDF_ERR_INVALID, "context is NULL");
+  if (n_lights < 0 || (n_lights > 0 && !lights)) return fail(NEDF_ERR_INVALID, "bad light list");
+  Frame F;
+  int rc = prepare_frame(ctx, cam, objs, n_objs, fields, n_fields, fb, F, st);
+  if (rc) return rc;
+  if ((rc = record(events, 0, st))) return rc;
+  const bool fuse = ctx->fuse && fb->planes_dev == nullptr;
+  rc = do_step1(ctx, F, st, !fuse);
+  if (rc) return rc;
+  if ((rc = record(events, 1, st))) return rc;
+  const bool shadows = cfg ? cfg->shadows != 0 : true;
+  const int nl = shadows ? n_lights : 0;
+  if (fuse) {
+    fill_config(F.fj, cfg);
+    F.fj.ray.mode = RAY_PRIMARY;
+    FrameJob sj = F.fj;
+    int smode = -1;
+    if (nl > 0 && (rc = make_shadow_job(ctx, F, objs, lights, cfg, sj, smode))) return rc;
+    CUDA_TRY(cudaMemsetAsync(F.ls.count, 0, 64 * sizeof(int), st));
+    if (F.n_pix > 0)
+      LAUNCH(ctx, launch_resolve_shade(F.fj, F.gt, F.ls, sj, smode, ctx->setup_exact, ctx->n_sms, st));
+    if ((rc = record(events, 2, st))) return rc;
+    for (int i = 0; i < nl; ++i) {
+      rc = do_step3(ctx, F, objs, lights + i, cfg, st, i == nl - 1 ? fb->image_dev : nullptr, i == 0);
+      if (rc) return rc;
+    }
+    if (nl == 0 && fb->image_dev && F.n_pix > 0)
+      LAUNCH(ctx, launch_composite(fb->rgb_dev, fb->shadow_dev, fb->image_dev, F.n_pix, ctx->n_sms, st));
+  } else {
+    rc = do_step2(ctx, F, cfg, st);
+    if (rc) return rc;
+    if ((rc = record(events, 2, st))) return rc;
+    if (F.n_pix > 0) LAUNCH(ctx, launch_fill(fb->shadow_dev, F.n_pix, 1.0f, ctx->n_sms, st));
+    for (int i = 0; i < nl; ++i) {
+      rc = do_step3(ctx, F, objs, lights + i, cfg, st);
+      if (rc) return rc;
+    }
+    if (fb->image_dev && F.n_pix > 0)
+      LAUNCH(ctx, launch_composite(fb->rgb_dev, fb->shadow_dev, fb->image_dev, F.n_pix, ctx->n_sms, st));
+  }
+  return record(events, 3, st);
 }
 
 }  // namespace
@@ -597,6 +675,12 @@ int nedf_set_option(NedfContext* c, int key, int64_t v) {
       if (v != 0 && v != 4 && v != 8) return fail(NEDF_ERR_INVALID, "guard cluster size must be 0, 4 or 8");
       c->guard_cluster = (int)v;
       return NEDF_OK;
+    case NEDF_OPT_SETUP_EXACT:
+      c->setup_exact = v != 0;
+      return NEDF_OK;
+    case NEDF_OPT_FUSE:
+      c->fuse = v != 0;
+      return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }
@@ -610,6 +694,8 @@ int nedf_get_option(NedfContext* c, int key, int64_t* v) {
     case NEDF_OPT_PROFILE: *v = c->profile; return NEDF_OK;
     case NEDF_OPT_TC_KERNEL: *v = c->tc_kernel; return NEDF_OK;
     case NEDF_OPT_GUARD_CLUSTER: *v = c->guard_cluster; return NEDF_OK;
+    case NEDF_OPT_SETUP_EXACT: *v = c->setup_exact; return NEDF_OK;
+    case NEDF_OPT_FUSE: *v = c->fuse; return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }
@@ -640,6 +726,7 @@ int nedf_stats_slot(NedfContext* c, int slot, NedfStepStats* out) {
   out->resampled = (int64_t)h[1];
   out->evals = (int64_t)h[2];
   out->guarded = (int64_t)h[3];
+  out->exact_clips = (int64_t)h[4];
   return NEDF_OK;
 }
 
@@ -658,6 +745,7 @@ int nedf_read_stats(NedfContext* c, NedfStepStats* out, void* stream) {
   out->resampled = (int64_t)h[1];
   out->evals = (int64_t)h[2];
   out->guarded = (int64_t)h[3];
+  out->exact_clips = (int64_t)h[4];
   out->launches = c->launches;
   c->launches = 0;
   out->h2d_bytes = c->h2d_bytes;
@@ -1028,26 +1116,15 @@ int nedf_composite(NedfContext* ctx, NedfFrameBuffers* fb, int width, void* stre
 int nedf_render_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject* objs, int n_objs,
                       const NedfField* fields, int n_fields, const NedfLight* lights, int n_lights,
                       const NedfRenderConfig* cfg, NedfFrameBuffers* fb, void* stream) {
-  if (!ctx) return fail(NEDF_ERR_INVALID, "context is NULL");
-  cudaStream_t st = (cudaStream_t)stream;
-  Frame F;
-  int rc = prepare_frame(ctx, cam, objs, n_objs, fields, n_fields, fb, F, st);
-  if (rc) return rc;
-  rc = do_step1(ctx, F, st);
-  if (rc) return rc;
-  rc = do_step2(ctx, F, cfg, st);
-  if (rc) return rc;
-  LAUNCH(ctx, launch_fill(fb->shadow_dev, F.n_pix, 1.0f, ctx->n_sms, st));
-  bool shadows = cfg ? cfg->shadows != 0 : true;
-  if (shadows) {
-    for (int i = 0; i < n_lights; ++i) {
-      rc = do_step3(ctx, F, objs, lights + i, cfg, st);
-      if (rc) return rc;
-    }
-  }
-  if (fb->image_dev && F.n_pix > 0)
-    LAUNCH(ctx, launch_composite(fb->rgb_dev, fb->shadow_dev, fb->image_dev, F.n_pix, ctx->n_sms, st));
-  return NEDF_OK;
+  return render_frame(ctx, cam, objs, n_objs, fields, n_fields, lights, n_lights, cfg, fb, nullptr,
+                      (cudaStream_t)stream);
+}
+
+int nedf_render_frame_timed(NedfContext* ctx, const NedfCamera* cam, const NedfObject* objs, int n_objs,
+                            const NedfField* fields, int n_fields, const NedfLight* lights, int n_lights,
+                            const NedfRenderConfig* cfg, NedfFrameBuffers* fb, void* const* events, void* stream) {
+  return render_frame(ctx, cam, objs, n_objs, fields, n_fields, lights, n_lights, cfg, fb, events,
+                      (cudaStream_t)stream);
 }
 
 }  // extern "C"

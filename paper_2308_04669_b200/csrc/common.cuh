@@ -60,6 +60,9 @@ struct DevObj {
   int recompute;                    // STEP 1 with a plane cache: 1 = evaluate this object's plane
   int pad2;
   float bs_c[3], bs_r;              // NeDF objects: world-space bounding sphere of the relaxed box (fp32 pre-test)
+  // NeDF objects, fp32 copies for the setup kernels' certified fp32 slab clip (clip_hit_f32)
+  float Rf[9], Tf[3], inv_sf;       // R, T, 1/s
+  float bminf[3], bmaxf[3];         // the model's relaxed box
 };
 
 // Conservative fp32 rejection before the float64 slab clip: true only when the
@@ -213,7 +216,27 @@ __device__ __forceinline__ void sample_point(const DevModel& m, const double lo[
   for (int a = 0; a < 3; ++a) p[a] = ((lo[a] + t * ld[a]) - m.c[a]) / m.h[a];
 }
 
-// World ray of a work item for the given mode.  Returns false if the item has no ray.
+// Shadow ray of a receiver x = co + D cd (camera ray, STEP-1 depth) for the job's light.
+__device__ __forceinline__ void shadow_ray(const RayJob& job, const double co[3], const double cd[3], double D,
+                                           double o[3], double d[3]) {
+  double x[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) x[a] = co[a] + D * cd[a];
+  if (job.mode == RAY_POINT_SHADOW) {
+    // pipeline.py:385-388: dir = (x - L) / max(|x - L|, 1e-300), origin = L
+    double v[3] = {x[0] - job.light[0], x[1] - job.light[1], x[2] - job.light[2]};
+    double dist = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    double dn = dist > 1e-300 ? dist : 1e-300;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { o[a] = job.light[a]; d[a] = v[a] / dn; }
+  } else {
+    // pipeline.py:395-396: dir = -light_dir, origin = x + eps * dir
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { d[a] = -job.light[a]; o[a] = x[a] + job.eps * d[a]; }
+  }
+}
+
+// World ray of a work item for the given mode.
 __device__ __forceinline__ void item_world_ray(const RayJob& job, uint32_t pix, double o[3], double d[3]) {
   if (job.mode == RAY_WORLD || job.mode == RAY_LOCAL) {
 #pragma unroll
@@ -230,22 +253,7 @@ __device__ __forceinline__ void item_world_ray(const RayJob& job, uint32_t pix, 
     for (int a = 0; a < 3; ++a) { o[a] = co[a]; d[a] = cd[a]; }
     return;
   }
-  double D = job.depth64[pix];
-  double x[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) x[a] = co[a] + D * cd[a];
-  if (job.mode == RAY_POINT_SHADOW) {
-    // pipeline.py:385-388: dir = (x - L) / max(|x - L|, 1e-300), origin = L
-    double v[3] = {x[0] - job.light[0], x[1] - job.light[1], x[2] - job.light[2]};
-    double dist = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
-    double dn = dist > 1e-300 ? dist : 1e-300;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) { o[a] = job.light[a]; d[a] = v[a] / dn; }
-  } else {
-    // pipeline.py:395-396: dir = -light_dir, origin = x + eps * dir
-#pragma unroll
-    for (int a = 0; a < 3; ++a) { d[a] = -job.light[a]; o[a] = x[a] + job.eps * d[a]; }
-  }
+  shadow_ray(job, co, cd, job.depth64[pix], o, d);
 }
 
 // Local-space ray of an item against its object (model.py:310-311).

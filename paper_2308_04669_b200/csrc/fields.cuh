@@ -48,6 +48,11 @@ __device__ __forceinline__ double leaf_sdf(const NedfField& f, const double p[3]
 // positive scales, so a DFS with a running min handles unions and nested
 // transforms without recursion.
 __device__ inline double field_sdf(const NedfField* fields, int root, const double p0[3]) {
+  const NedfField& r = fields[root];
+  if (r.kind != NEDF_FIELD_UNION && r.kind != NEDF_FIELD_TRANSFORMED) {   // a single primitive: no DFS stack
+    const double v = leaf_sdf(r, p0);
+    return v < INFINITY ? v : INFINITY;
+  }
   struct Frame { int node; double p[3]; double scale; };
   Frame st[12];
   int sp = 0;

@@ -31,15 +31,21 @@ struct FrameJob {
   double sigma_threshold;        // < 0: per-field default
   int resample, resample_samples;
   double clear[3];
-  unsigned long long* stats;     // [0] covered, [1] outliers
+  unsigned long long* stats;     // [0] covered, [1] outliers, [2] evals, [3] guarded, [4] exact box tests
 };
 
-cudaError_t launch_setup(const FrameJob& fj, const GroupTable& gt, const ListSet& ls, int mode, int n_sms,
+// exact = 1: every box test in float64 (no certified fp32 clip)
+cudaError_t launch_setup(const FrameJob& fj, const GroupTable& gt, const ListSet& ls, int mode, int exact, int n_sms,
                          cudaStream_t st);
+// fused STEP 1 resolve + STEP 2 + shadow := 1 + STEP 3 lists of the first light (smode < 0: none)
+cudaError_t launch_resolve_shade(const FrameJob& fj, const GroupTable& gt, const ListSet& ls, const FrameJob& sj,
+                                 int smode, int exact, int n_sms, cudaStream_t st);
 cudaError_t launch_step1_resolve(const FrameJob& fj, const GroupTable& gt, int n_sms, cudaStream_t st);
 cudaError_t launch_recombine(const FrameJob& fj, int n_sms, cudaStream_t st);
 cudaError_t launch_shade(const FrameJob& fj, const GroupTable& gt, int n_sms, cudaStream_t st);
-cudaError_t launch_shadow_resolve(const FrameJob& fj, const GroupTable& gt, int mode, int n_sms, cudaStream_t st);
+// image != NULL: also image = rgb * shadow (the frame's last light)
+cudaError_t launch_shadow_resolve(const FrameJob& fj, const GroupTable& gt, int mode, float* image, int n_sms,
+                                  cudaStream_t st);
 cudaError_t launch_fill(float* buf, int64_t n, float v, int n_sms, cudaStream_t st);
 cudaError_t launch_composite(const float* rgb, const float* shadow, float* image, int64_t n, int n_sms,
                              cudaStream_t st);
@@ -82,7 +88,7 @@ cudaError_t launch_stats_export(unsigned long long* stats, unsigned long long* h
 bool tc_available();
 // csize = CTAs per cluster sharing one multicast weight stream (1, 2 or 4)
 cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, int csize, cudaStream_t stream);
-// CTA-pair variant (mlp_tc2.cu): same contract, 256-ray tiles on SM pairs; n_ctas is rounded down to even
+// one-time fp16 operand image of a paper-shaped model for the tensor-core kernel
 cudaError_t tc_pack_weights(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
                             __half** wpack_dev, float** bias_dev, size_t* bytes);
 

@@ -497,27 +497,45 @@ def compose_frame(scene, camera: Camera, lights, config: RenderConfig | None = N
     ctx = _ctx(buffers)
     st = _lib.stream_handle()
     ctx.reset_stats(st)                    # zero the per-frame counters (no sync)
-    ev[0].record()
-    if changed_ids is None:
-        nedf_generation_step(scene, camera, buffers, _tables=tb)
+    if changed_ids is None and external is None:
+        # the whole frame in one call (the library fuses the per-pixel passes); events at the step
+        # boundaries (the STEP 1 resolve and the first light's shadow-ray setup run in the STEP 2 pass)
+        for e in ev:
+            e.record()                     # torch creates its events lazily, on first record
+        handles = (C.c_void_p * 4)(*[e.cuda_event for e in ev])
+        lights = list(lights) if config.shadows else []
+        lc = (_lib.NedfLight * max(1, len(lights)))(*[_light_c(L) for L in lights])
+        cfg_c = config._c()
+        _lib.check(_lib.load_library().nedf_render_frame_timed(
+            ctx.handle, C.byref(camera._c()), tb.objs, tb.n_objs, tb.fields, tb.n_fields, lc, len(lights),
+            C.byref(cfg_c), C.byref(buffers._c(tb.n_objs)), handles, st))
+        _publish_planes(scene, buffers)
     else:
-        reuse_buffers(scene, camera, buffers, changed_ids, _tables=tb)
-    ev[1].record()
-    if external is not None:
-        import_external_gbuffer(buffers, external[0], external[1], external[2])
-    deferred_shading_step(scene, camera, buffers, config, _tables=tb, _stats=False)
-    ev[2].record()
-    buffers.shadow.fill_(1.0)
-    if config.shadows:
-        for light in lights:
-            shadow_step(scene, camera, buffers, light, config, _tables=tb)
-    _lib.check(_lib.load_library().nedf_composite(ctx.handle, C.byref(buffers._c(tb.n_objs)), camera.width, st))
+        ev[0].record()
+        if changed_ids is None:
+            nedf_generation_step(scene, camera, buffers, _tables=tb)
+        else:
+            reuse_buffers(scene, camera, buffers, changed_ids, _tables=tb)
+        ev[1].record()
+        if external is not None:
+            import_external_gbuffer(buffers, external[0], external[1], external[2])
+        deferred_shading_step(scene, camera, buffers, config, _tables=tb, _stats=False)
+        ev[2].record()
+        buffers.shadow.fill_(1.0)
+        if config.shadows:
+            for light in lights:
+                shadow_step(scene, camera, buffers, light, config, _tables=tb)
+        _lib.check(_lib.load_library().nedf_composite(ctx.handle, C.byref(buffers._c(tb.n_objs)), camera.width,
+                                                      st))
+    if changed_ids is not None or external is not None:
+        ev[3].record()
     slot, host = ctx.snapshot_stats(st)
-    ev[3].record()
+    done = torch.cuda.Event()
+    done.record()
     n_pix = float(camera.width * buffers.n_rows)
 
     def resolve():
-        ev[3].synchronize()
+        done.synchronize()
         dev = ctx.slot_stats(slot)
         return {
             "step1_depth_id": ev[0].elapsed_time(ev[1]) / 1e3,

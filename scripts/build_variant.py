@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Build an experimental variant of the library: recompile one source with
-extra -D flags and link it with the regular objects into _exp/<name>.so.
-Load it with NEDF_LIB=_exp/<name>.so (timing experiments only)."""
+extra -D flags and link it with the regular objects into _var/<name>.so.
+Load it with NEDF_LIB=_var/<name>.so (timing experiments only)."""
 import subprocess
 import sys
 from pathlib import Path
@@ -12,7 +12,7 @@ from paper_2308_04669_b200 import build as B  # noqa: E402
 
 name, src, *defs = sys.argv[1:]
 B.build()
-out_dir = ROOT / "_exp"
+out_dir = ROOT / "_var"   # git-ignored (*.so) but not gpurun-ignored: travels to the GPU box
 out_dir.mkdir(exist_ok=True)
 src = Path(src) if Path(src).is_absolute() else B.CSRC / src   # an absolute path replaces csrc/<same stem>.cu
 obj = out_dir / f"{name}_{src.stem}.o"

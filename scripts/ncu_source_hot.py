@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Hottest source lines (warp-stall samples, top stall reasons) of an ncu report
-captured with --import-source on.  usage: ncu_source_hot.py REPORT [N] [file-substring]"""
+captured with --import-source on.  usage: ncu_source_hot.py REPORT [N] [file-substring] [inst]"""
 import csv
 import subprocess
 import sys
@@ -39,7 +39,8 @@ def num(x):
 
 tot = sum(num(m[st]) for *_, m in out)
 print("total stall samples", tot)
-rows = sorted([o for o in out if filt in o[0]], key=lambda o: -num(o[3][st]))[:N]
+key = ie if (len(sys.argv) > 4 and sys.argv[4] == "inst") else st     # sort by stall samples or instructions
+rows = sorted([o for o in out if filt in o[0]], key=lambda o: -num(o[3][key]))[:N]
 for fn, ln, t, m in rows:
     s = num(m[st])
     rs = sorted(((num(m[Hm.index(k)]), k[6:]) for k in reasons), reverse=True)[:3]
