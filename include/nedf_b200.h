@@ -67,9 +67,16 @@ enum {
   NEDF_OPT_GUARD_CLUSTER = 6,   /* near-tie guard kernel's cluster size: 4, 8, or 0 = by frame size */
   NEDF_OPT_SETUP_EXACT = 7,     /* 1 = every work-list box test in float64 (default 0: certified fp32 test,
                                    float64 only where its error bound cannot decide; same lists either way) */
-  NEDF_OPT_FUSE = 8             /* 1 (default) = nedf_render_frame fuses the per-pixel passes (STEP 1 resolve,
+  NEDF_OPT_FUSE = 8,            /* 1 (default) = nedf_render_frame fuses the per-pixel passes (STEP 1 resolve,
                                    STEP 2, shadow fill, first light's STEP 3 setup; last light's resolve +
                                    composite); 0 = one kernel per step, as the step entry points run */
+  NEDF_OPT_GUARD_KERNEL = 9     /* one of NEDF_GUARD_*: which kernel re-evaluates the near-tie rays */
+};
+/* Near-tie guard kernels (NEDF_OPT_GUARD_KERNEL); both fp32-accurate. */
+enum {
+  NEDF_GUARD_AUTO = 0,      /* NEDF_GUARD_TCGEN05 */
+  NEDF_GUARD_TCGEN05 = 1,   /* tcgen05 tf32 + bf16 split products, 4-CTA clusters (guard_tc.cu) */
+  NEDF_GUARD_MMA_SYNC = 2   /* warp-level mma.sync 3xTF32, 4- or 8-CTA clusters (mlp_fp32c.cu) */
 };
 
 /* Tensor-core network kernels (NEDF_OPT_TC_KERNEL). */

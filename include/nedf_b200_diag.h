@@ -21,8 +21,15 @@ extern "C" {
 int nedf_diag_umma(const void* a_dev, const void* b_dev, float* d_dev, int k, int n, int a_in_tmem, int d_col,
                    void* stream);
 
+/* One-CTA kind::tf32 (bf16 = 0) or kind::f16 bf16 (bf16 = 1) tcgen05 GEMM of fp32 A[m][k],
+ * B[n][k] (m = 64 or 128), SW128 K-major: writes the raw accumulator, TMEM lanes 0..127 x
+ * n columns, to draw[128][n] (pins the M = 64 layout of the guard kernel). */
+int nedf_diag_umma32(const float* a_dev, const float* b_dev, float* draw_dev, int m, int n, int k, int bf16,
+                     void* stream);
+
 /* Raw network logits for local rays (rows that miss the box are left
- * untouched): precision NEDF_PREC_TENSOR (tcgen05 kernel) or NEDF_PREC_FP32. */
+ * untouched): precision NEDF_PREC_TENSOR (tcgen05 kernel), NEDF_PREC_FP32, or
+ * 16 + NEDF_GUARD_* (only that near-tie guard kernel, on every ray). */
 int nedf_diag_ray_logits(NedfContext* ctx, const NedfModel* m, const double* origins_dev, const double* dirs_dev,
                          int64_t n, float* coarse_dev, float* fine_dev, float* alpha_logit_dev, int precision,
                          void* stream);
@@ -38,6 +45,11 @@ int nedf_diag_tc_trace(int enable, unsigned long long* out, int n);
  * per tile i < 4, [64 i] start, [64 i + 1] rays set up, [64 i + 2] features
  * landed, [64 i + 3 + L] layer L landed, [64 i + 40] decoded; n <= 256. */
 int nedf_diag_cl_trace(int enable, unsigned long long* out, int n);
+
+/* Timeline of cluster 0 / CTA 0's first tile in the tcgen05 guard kernel (clock64): [L] layer
+ * L's MMAs start, [40+L] issued, [80+L] epilogue has the accumulators, [120+L] slab sent,
+ * [160+L] layer landed, [200+L] next B tiles written, [240+q] weight stage q issued; n <= 320. */
+int nedf_diag_guard_trace(int enable, unsigned long long* out, int n);
 
 /* tcgen05 issue-rate probe: `iters` M=128 x N MMAs (ts: A from TMEM) from one
  * warp, committing every `per_commit`; writes elapsed clock64 cycles to out_dev. */

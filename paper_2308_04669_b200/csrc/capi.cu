@@ -61,6 +61,7 @@ struct NedfModel {
   float* wstream = nullptr;
   float* wcluster = nullptr;
   float* wcluster8 = nullptr;
+  void* wguard = nullptr;
   int device = 0;
 };
 
@@ -74,8 +75,10 @@ struct NedfContext {
   int tc_ctas = 0;
   int tc_kernel = NEDF_TC_AUTO;
   int guard_cluster = 0;
+  int guard_kernel = NEDF_GUARD_AUTO;
   int setup_exact = 0;
   int fuse = 1;
+  int guard_direct = 0;      // diagnostics: run only the guard kernel NEDF_GUARD_* on every list entry
   int profile = 0;
   int64_t launches = 0;
   // event pairs around network launches (NEDF_OPT_PROFILE); kind 0 = main, 1 = guard
@@ -404,6 +407,11 @@ int prof_mark(NedfContext* ctx, cudaStream_t st, int kind, bool start) {
 // Evaluate the network on every list entry with the context's precision.
 int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& out, cudaStream_t st) {
   if (F.gt.n_groups == 0) return NEDF_OK;
+  if (ctx->guard_direct) {
+    if (ctx->guard_direct == NEDF_GUARD_TCGEN05) LAUNCH(ctx, launch_guard_tc(F.gt, F.ls, job, out, ctx->n_sms, st));
+    else LAUNCH(ctx, launch_mlp_fp32_cluster(F.gt, F.ls, job, out, ctx->n_sms, ctx->guard_cluster ? ctx->guard_cluster : 4, st));
+    return NEDF_OK;
+  }
   bool use_tc = ctx->precision != NEDF_PREC_FP32 && F.sc.all_tc && tc_available();
   int rc;
   if (use_tc) {
@@ -427,9 +435,13 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
       // 8-CTA clusters halve the MMA work per layer on a CTA's critical path but only ~18 fit at
       // once (vs ~33 of 4): by default they take frames with at most half a 2000 x 800 x 8-object
       // frame's (pixel, object) pairs, whose guard batch then still fits one round
-      int cl = ctx->guard_cluster;
-      if (cl == 0) cl = (int64_t)F.n_pix * F.sc.n_objs <= 6400000 ? 8 : 4;
-      LAUNCH(ctx, launch_mlp_fp32_cluster(F.gt, F.redo, job, out, ctx->n_sms, cl, st));
+      if (ctx->guard_kernel != NEDF_GUARD_MMA_SYNC && guard_tc_available()) {
+        LAUNCH(ctx, launch_guard_tc(F.gt, F.redo, job, out, ctx->n_sms, st));
+      } else {
+        int cl = ctx->guard_cluster;
+        if (cl == 0) cl = (int64_t)F.n_pix * F.sc.n_objs <= 6400000 ? 8 : 4;
+        LAUNCH(ctx, launch_mlp_fp32_cluster(F.gt, F.redo, job, out, ctx->n_sms, cl, st));
+      }
       if ((rc = prof_mark(ctx, st, 1, false))) return rc;
     }
     add_counts_kernel<<<1, 32, 0, st>>>(F.ls.count, F.redo.count, F.gt.n_groups, F.fj.stats, a.use_guard);
@@ -678,6 +690,11 @@ int nedf_set_option(NedfContext* c, int key, int64_t v) {
     case NEDF_OPT_SETUP_EXACT:
       c->setup_exact = v != 0;
       return NEDF_OK;
+    case NEDF_OPT_GUARD_KERNEL:
+      if (v != NEDF_GUARD_AUTO && v != NEDF_GUARD_TCGEN05 && v != NEDF_GUARD_MMA_SYNC)
+        return fail(NEDF_ERR_INVALID, "bad guard kernel");
+      c->guard_kernel = (int)v;
+      return NEDF_OK;
     case NEDF_OPT_FUSE:
       c->fuse = v != 0;
       return NEDF_OK;
@@ -695,6 +712,7 @@ int nedf_get_option(NedfContext* c, int key, int64_t* v) {
     case NEDF_OPT_TC_KERNEL: *v = c->tc_kernel; return NEDF_OK;
     case NEDF_OPT_GUARD_CLUSTER: *v = c->guard_cluster; return NEDF_OK;
     case NEDF_OPT_SETUP_EXACT: *v = c->setup_exact; return NEDF_OK;
+    case NEDF_OPT_GUARD_KERNEL: *v = c->guard_kernel; return NEDF_OK;
     case NEDF_OPT_FUSE: *v = c->fuse; return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
@@ -835,6 +853,7 @@ int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* 
     if (m->wstream) cudaFree(m->wstream);
     if (m->wcluster) cudaFree(m->wcluster);
     if (m->wcluster8) cudaFree(m->wcluster8);
+    if (m->wguard) cudaFree(m->wguard);
     if (m->dev) cudaFree(m->dev);
     delete m;
   };
@@ -867,6 +886,9 @@ int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* 
     if (e != cudaSuccess) { cleanup(); return fail(NEDF_ERR_CUDA, std::string("fp32 pack: ") + cudaGetErrorString(e)); }
     h.wcluster = m->wcluster;
     h.wcluster8 = m->wcluster8;
+    e = guard_tc_pack(params, info->d_in, F, info->n_blocks, info->n_coarse, info->n_fine, &m->wguard);
+    if (e != cudaSuccess) { cleanup(); return fail(NEDF_ERR_CUDA, std::string("guard pack: ") + cudaGetErrorString(e)); }
+    h.wguard = m->wguard;
     h.tensor_ok = 1;
   }
   e = cudaMalloc(&m->dev, sizeof(DevModel));
@@ -915,6 +937,7 @@ void nedf_model_free(NedfModel* m) {
   if (m->wstream) cudaFree(m->wstream);
   if (m->wcluster) cudaFree(m->wcluster);
   if (m->wcluster8) cudaFree(m->wcluster8);
+  if (m->wguard) cudaFree(m->wguard);
   if (m->dev) cudaFree(m->dev);
   delete m;
 }
@@ -1040,8 +1063,13 @@ extern "C" int nedf_diag_ray_logits(NedfContext* ctx, const NedfModel* m, const 
   if (precision == NEDF_PREC_TENSOR && !m->host.tensor_ok) return fail(NEDF_ERR_UNSUPPORTED, "model not tensor-core shaped");
   int saved = ctx->precision;
   ctx->precision = precision == NEDF_PREC_TENSOR ? NEDF_PREC_TENSOR : NEDF_PREC_FP32;
+  if (precision == 16 + NEDF_GUARD_TCGEN05 || precision == 16 + NEDF_GUARD_MMA_SYNC) {
+    if (!m->host.tensor_ok) return fail(NEDF_ERR_UNSUPPORTED, "model not tensor-core shaped");
+    ctx->guard_direct = precision - 16;
+  }
   int rc = query_common(ctx, m, RAY_LOCAL, nullptr, nullptr, 1.0, o, d, n, nullptr, nullptr, (cudaStream_t)stream,
                         lc, lf, la);
+  ctx->guard_direct = 0;
   ctx->precision = saved;
   return rc;
 }

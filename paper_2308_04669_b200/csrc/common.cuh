@@ -40,6 +40,7 @@ struct DevModel {
   const float* wstream;          // fp32 stream image for mlp_fp32s.cu (paper-shaped models)
   const float* wcluster;         // fp32 cluster-split images for mlp_fp32c.cu (paper-shaped models):
   const float* wcluster8;        //   4-CTA and 8-CTA clusters
+  const void* wguard;            // tcgen05 guard image (guard_tc.cu, paper-shaped models)
   int64_t wT_off[40];            // layer offsets into wT  (n_layers <= 35 for the paper profile; general cap 40)
   int64_t b_off[40];
   int n_layers;

@@ -83,6 +83,12 @@ struct TcArgs {
   int use_guard;
   int* tile_counter;
 };
+// tcgen05 guard (guard_tc.cu): fp32-accurate re-evaluation of `ls` (the redo list) in 4-CTA clusters
+bool guard_tc_available();
+cudaError_t launch_guard_tc(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
+                            int n_sms, cudaStream_t stream);
+cudaError_t guard_tc_pack(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
+                          void** dev);
 // copy the 8 frame counters to mapped host memory and clear them (nedf_read_stats)
 cudaError_t launch_stats_export(unsigned long long* stats, unsigned long long* host_mapped, cudaStream_t st);
 bool tc_available();

@@ -4,6 +4,8 @@
 // the 32x32b TMEM load of the fp32 accumulator.
 #include <cstdio>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 #include "../../include/nedf_b200_diag.h"
@@ -101,6 +103,86 @@ extern "C" int nedf_diag_umma(const void* a, const void* b, float* d, int k, int
   cudaFuncSetAttribute(umma_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   umma_unit_kernel<<<1, 128, smem, (cudaStream_t)stream>>>((const __half*)a, (const __half*)b, d, k, n, a_in_tmem,
                                                            d_col);
+  return cudaGetLastError() == cudaSuccess ? NEDF_OK : NEDF_ERR_CUDA;
+}
+
+namespace nedf {
+
+// kind::tf32 / kind::f16(bf16) unit GEMM, A [M][K] and B [N][K] given as fp32 (bf16: rounded
+// on staging), 128B-swizzled K-major tiles of 32 fp32 (or 64 bf16) K per atom; writes the raw
+// TMEM accumulator, all 128 lanes x N columns, to Draw[lane][n] (pins the M = 64 D layout).
+__global__ void __launch_bounds__(128, 1)
+umma32_unit_kernel(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ Draw, int M, int N,
+                   int K, int bf16, int d_lane) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int esz = bf16 ? 2 : 4, per_atom = 128 / esz, n_atoms = K / per_atom;
+  unsigned char* sa = smem;                            // n_atoms x [M rows x 128 B]
+  unsigned char* sb = smem + (size_t)n_atoms * M * 128;
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int e = tid; e < (M + N) * K; e += 128) {
+    const bool isa = e < M * K;
+    const int r = isa ? e / K : (e - M * K) / K, k = isa ? e % K : (e - M * K) % K;
+    const float v = isa ? A[(size_t)r * K + k] : B[(size_t)r * K + k];
+    const int atom = k / per_atom, kin = k % per_atom;
+    unsigned char* base = (isa ? sa + (size_t)atom * M * 128 : sb + (size_t)atom * N * 128);
+    const uint32_t off = tc::sw128_offset(r, (kin * esz) >> 4) + ((kin * esz) & 15);
+    if (bf16) *reinterpret_cast<__nv_bfloat16*>(base + off) = __float2bfloat16_rn(v);
+    else *reinterpret_cast<float*>(base + off) = v;
+  }
+  tc::fence_proxy_async_smem();
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base_s);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = tmem_base_s;
+  if (tid == 0) {
+    const uint32_t idesc = bf16 ? tc::idesc_bf16(M, N) : tc::idesc_tf32(M, N);
+    const int steps = K / (bf16 ? 16 : 8);
+    for (int s = 0; s < steps; ++s) {
+      const int atom = s / 4, within = (s % 4) * 32;
+      const uint64_t ad = tc::sw128_desc(tc::smem_u32(sa + (size_t)atom * M * 128) + within);
+      const uint64_t bd = tc::sw128_desc(tc::smem_u32(sb + (size_t)atom * N * 128) + within);
+      const uint32_t dt = tbase + ((uint32_t)d_lane << 16);
+      if (bf16) tc::mma_ss(dt, ad, bd, idesc, s > 0);
+      else tc::mma_ss_tf32(dt, ad, bd, idesc, s > 0);
+    }
+    tc::mma_commit(&bar);
+  }
+  __syncwarp();
+  tc::mbar_wait(&bar, 0);
+  tc::tc_fence_after();
+  for (int c0 = 0; c0 < N; c0 += 8) {
+    uint32_t r[8];
+    tc::tmem_ld8(tbase + ((uint32_t)(warp * 32) << 16) + c0, r);
+    tc::tmem_ld_wait();
+    for (int j = 0; j < 8; ++j) Draw[(size_t)tid * N + c0 + j] = __uint_as_float(r[j]);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tbase);
+}
+
+}  // namespace nedf
+
+extern "C" int nedf_diag_umma32(const float* a, const float* b, float* draw, int m, int n, int k, int bf16,
+                                void* stream) {
+  using namespace nedf;
+  const int d_lane = bf16 >> 8;                 // bits 8+: TMEM lane offset of the accumulator (layout probe)
+  bf16 &= 0xFF;
+  const int per_atom = bf16 ? 64 : 32;
+  if (!a || !b || !draw || (m != 64 && m != 128) || n < 8 || n > 256 || n % 8 || k < per_atom || k > 256 ||
+      k % per_atom)
+    return NEDF_ERR_INVALID;
+  const size_t smem = (size_t)(k / per_atom) * (m + n) * 128 + 1024;
+  cudaFuncSetAttribute(umma32_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  umma32_unit_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(a, b, draw, m, n, k, bf16, d_lane);
   return cudaGetLastError() == cudaSuccess ? NEDF_OK : NEDF_ERR_CUDA;
 }
 

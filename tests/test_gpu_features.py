@@ -213,39 +213,6 @@ def test_frames_are_deterministic(P):
     np.testing.assert_array_equal(i1, r2.image.cpu().numpy())
 
 
-@pytest.mark.parametrize("cluster", [4, 8])
-@pytest.mark.parametrize("n_rays", [3000, 300, 60])
-def test_cluster_guard_kernel_matches_fp32_path(P, n_rays, cluster):
-    """With the guard threshold at 100% of max|logit| every ray is re-evaluated
-    by the cluster-split fp32 kernel (mlp_fp32c.cu); its decisions must match
-    the streaming fp32 kernel's (NEDF_PREC_FP32) up to fp32 summation-order
-    ties, and its depths must agree to float32 accuracy.  3000 rays take several
-    rounds of 16-ray tiles, 300 and 60 one round; both cluster shapes (4 CTAs x
-    64 columns, 8 CTAs x 32 columns with K split across warp pairs)."""
-    _lib, fields, geometry, model, pipeline, scenes = _mods()
-    ctx = _lib.context()
-    m = scenes.paper_model(1, "box")
-    o, d = CF.sweep_rays(n_rays, m.relaxed_box.min, m.relaxed_box.max, seed=11)
-    ctx.set_option(_lib.OPT_PRECISION, _lib.PREC_FP32)
-    mu32, a32 = model.query_rays(m, o, d)
-    ctx.set_option(_lib.OPT_PRECISION, _lib.PREC_AUTO)
-    ctx.set_option(_lib.OPT_GUARD_PPM, 1_000_000)
-    ctx.set_option(_lib.OPT_GUARD_CLUSTER, cluster)
-    try:
-        mug, ag = model.query_rays(m, o, d)
-    finally:
-        ctx.set_option(_lib.OPT_GUARD_PPM, 3000)
-        ctx.set_option(_lib.OPT_GUARD_CLUSTER, 0)
-    allowed = max(1, n_rays // 1000)        # fp32 summation-order near-ties
-    assert (ag != a32).sum() <= allowed
-    fin = np.isfinite(mu32) & np.isfinite(mug)
-    same = np.abs(mug[fin] - mu32[fin]) <= 1e-12
-    assert (~same).sum() <= allowed
-    # a differing ray differs by one fine bin at most (fp32 near-tie)
-    fine = 2 * m.config.half_range / m.n_coarse / m.n_fine
-    assert np.all(np.abs(mug[fin] - mu32[fin]) <= fine * 1.0001 + 2 * m.config.half_range / m.n_coarse)
-
-
 def test_precision_modes_agree_on_decisions(P):
     _lib, fields, geometry, model, pipeline, scenes = _mods()
     scene, cam, lights, cfg = scenes.build(CF.config4(300, 120))
