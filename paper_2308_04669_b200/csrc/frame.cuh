@@ -89,6 +89,10 @@ cudaError_t launch_guard_tc(const GroupTable& gt, const ListSet& ls, const RayJo
                             int n_sms, cudaStream_t stream);
 cudaError_t guard_tc_pack(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
                           void** dev);
+// fp32-accurate split-tf32 tcgen05 GEMM (train_gemm.cu): C[M][N] (+)= op(A)[M][K] op(B)[N][K]^T,
+// ta / tb: operand stored transposed; ws (optional) for split K over the CTAs
+cudaError_t gemm_tf32x3(const float* A, int lda, int ta, const float* B, int ldb, int tb, float* C, int ldc, int M,
+                        int N, int K, float beta, float* ws, size_t ws_floats, int n_sms, cudaStream_t st);
 // copy the 8 frame counters to mapped host memory and clear them (nedf_read_stats)
 cudaError_t launch_stats_export(unsigned long long* stats, unsigned long long* host_mapped, cudaStream_t st);
 bool tc_available();

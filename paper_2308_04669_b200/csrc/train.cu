@@ -10,11 +10,11 @@
 //   backward  exact reverse mode (nn.py:138-167)
 //   update    Adam with bias correction (nn.py:218-232)
 //
-// The matrix products are plain fp32 GEMMs and go to cuBLAS (SGEMM, no TF32, so
-// gradients stay fp32-exact for the finite-difference-style parity tests); the
-// encoding, tracing, targets, bias / activation epilogues, loss, column sums and
-// the Adam update are the kernels below.
-#include <cublas_v2.h>
+// The matrix products run on the tensor cores as fp32-accurate split tf32 GEMMs
+// (train_gemm.cu: hi / lo operand split, three tcgen05 MMAs per k-step, so the
+// gradients stay at fp32 accuracy for the parity tests); the encoding, tracing,
+// targets, bias / activation epilogues, loss, column sums and the Adam update are
+// the kernels below.
 
 #include <cmath>
 #include <cstring>
@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "encode.cuh"
+#include "frame.cuh"
 #include "fields.cuh"
 #include "../../include/nedf_b200.h"
 
@@ -81,11 +82,7 @@ int tfail(int code, const std::string& msg) {
     cudaError_t e_ = (expr);                                                            \
     if (e_ != cudaSuccess) return tfail(NEDF_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
   } while (0)
-#define BTRY(expr)                                                                      \
-  do {                                                                                  \
-    cublasStatus_t s_ = (expr);                                                         \
-    if (s_ != CUBLAS_STATUS_SUCCESS) return tfail(NEDF_ERR_CUDA, std::string(#expr ": cuBLAS status ") + std::to_string((int)s_)); \
-  } while (0)
+#define BTRY(expr) TTRY(expr)
 
 int blocks(int64_t n, int per = 256) {
   const int64_t b = (n + per - 1) / per;
@@ -223,20 +220,32 @@ __global__ void relu_mask_kernel(const float* __restrict__ a, const float* __res
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = a[i] > 0.f ? g[i] : 0.f;
 }
-// db[c] = sum_r g[r][c]  (one block per 32 columns; rows strided over the block's 8 warps)
-__global__ void colsum_kernel(const float* __restrict__ g, int rows, int cols, float* __restrict__ db) {
-  __shared__ float part[8][33];
+// db[c] = sum_r g[r][c] in two deterministic passes: block (column block, row slice) sums its
+// slice into part[slice][c] (8 warps striding the slice's rows, then a fixed-order combine),
+// then colsum_final adds the slices in order
+constexpr int kColSlices = 64;
+__global__ void colsum_partial_kernel(const float* __restrict__ g, int rows, int cols, int rows_per_slice,
+                                      float* __restrict__ part) {
+  __shared__ float acc[8][33];
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5;
+  const int r0 = blockIdx.y * rows_per_slice, r1 = min(rows, r0 + rows_per_slice);
   float s = 0.f;
   if (c < cols)
-    for (int r = w; r < rows; r += 8) s += g[(size_t)r * cols + c];
-  part[w][threadIdx.x & 31] = s;
+    for (int r = r0 + w; r < r1; r += 8) s += g[(size_t)r * cols + c];
+  acc[w][threadIdx.x & 31] = s;
   __syncthreads();
   if (w == 0 && c < cols) {
     float t = 0.f;
-    for (int k = 0; k < 8; ++k) t += part[k][threadIdx.x];
-    db[c] = t;
+    for (int k = 0; k < 8; ++k) t += acc[k][threadIdx.x];
+    part[(size_t)blockIdx.y * cols + c] = t;
   }
+}
+__global__ void colsum_final_kernel(const float* __restrict__ part, int slices, int cols, float* __restrict__ db) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float t = 0.f;
+  for (int k = 0; k < slices; ++k) t += part[(size_t)k * cols + c];
+  db[c] = t;
 }
 // Adam (nn.py:218-232)
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
@@ -265,7 +274,8 @@ struct NedfTrainer {
   int cap = 0, n = 0, n_valid = 0;
   double l = 1.0;
   Box box;
-  cublasHandle_t blas = nullptr;
+  int n_sms = 148;
+  DBuf<float> ws;                                // split-K workspace of the weight-gradient GEMMs
   DBuf<float> params, grads, m, v;
   DBuf<float> feats, xs, a1, h1, a2, la65, lf, gx, gtmp, g2;
   DBuf<double> o, d, sums;
@@ -277,20 +287,28 @@ struct NedfTrainer {
 
 namespace {
 
-// Y[rows][N] = X[rows][K] . W[N][K]^T  (row-major)
-cublasStatus_t gemm_xwT(cublasHandle_t h, const float* X, const float* W, float* Y, int rows, int N, int K) {
-  const float one = 1.f, zero = 0.f;
-  return cublasSgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, N, rows, K, &one, W, K, X, K, &zero, Y, N);
+constexpr size_t kWsFloats = (size_t)1 << 22;   // 16 MB
+
+cudaError_t colsum(NedfTrainer* t, const float* g, int rows, int cols, float* db, cudaStream_t st) {
+  const int per = (rows + kColSlices - 1) / kColSlices;
+  const int slices = (rows + per - 1) / per;
+  colsum_partial_kernel<<<dim3((cols + 31) / 32, slices), 256, 0, st>>>(g, rows, cols, per, t->ws.p);
+  colsum_final_kernel<<<(cols + 127) / 128, 128, 0, st>>>(t->ws.p, slices, cols, db);
+  return cudaGetLastError();
 }
-// dW[N][K] = G[rows][N]^T . X[rows][K]
-cublasStatus_t gemm_gTx(cublasHandle_t h, const float* G, const float* X, float* dW, int rows, int N, int K) {
-  const float one = 1.f, zero = 0.f;
-  return cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, K, N, rows, &one, X, K, G, N, &zero, dW, K);
+
+// Y[rows][N] = X[rows][K] . W[N][K]^T  (row-major)
+cudaError_t gemm_xwT(NedfTrainer* t, const float* X, const float* W, float* Y, int rows, int N, int K, cudaStream_t st) {
+  return gemm_tf32x3(X, K, 0, W, K, 0, Y, N, rows, N, K, 0.f, nullptr, 0, t->n_sms, st);
+}
+// dW[N][K] = G[rows][N]^T . X[rows][K]  (reduction over the batch: split K)
+cudaError_t gemm_gTx(NedfTrainer* t, const float* G, const float* X, float* dW, int rows, int N, int K, cudaStream_t st) {
+  return gemm_tf32x3(G, N, 1, X, K, 1, dW, K, N, K, rows, 0.f, t->ws.p, t->ws.n, t->n_sms, st);
 }
 // dX[rows][K] (+)= G[rows][N] . W[N][K]
-cublasStatus_t gemm_gW(cublasHandle_t h, const float* G, const float* W, float* dX, int rows, int N, int K, float beta) {
-  const float one = 1.f;
-  return cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, K, rows, N, &one, W, K, G, N, &beta, dX, K);
+cudaError_t gemm_gW(NedfTrainer* t, const float* G, const float* W, float* dX, int rows, int N, int K, float beta,
+                    cudaStream_t st) {
+  return gemm_tf32x3(G, N, 0, W, K, 1, dX, K, rows, K, N, beta, nullptr, 0, t->n_sms, st);
 }
 
 }  // namespace
@@ -339,12 +357,13 @@ extern "C" int nedf_trainer_create(int device, const NedfModelInfo* info, const 
   if (e == cudaSuccess) e = t->tc.ensure(B);
   if (e == cudaSuccess) e = t->tf.ensure(B);
   if (e == cudaSuccess) e = t->valid.ensure(B);
+  if (e == cudaSuccess) e = t->ws.ensure(kWsFloats);
   if (e == cudaSuccess) e = cudaMemcpy(t->params.p, params_host, P * sizeof(float), cudaMemcpyHostToDevice);
-  if (e != cudaSuccess || cublasCreate(&t->blas) != CUBLAS_STATUS_SUCCESS) {
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&t->n_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) {
     nedf_trainer_destroy(t);
     return tfail(NEDF_ERR_CUDA, std::string("trainer allocation: ") + cudaGetErrorString(e));
   }
-  cublasSetMathMode(t->blas, CUBLAS_PEDANTIC_MATH);   // true fp32 products (no TF32)
   *out = t;
   return NEDF_OK;
 }
@@ -352,8 +371,7 @@ extern "C" int nedf_trainer_create(int device, const NedfModelInfo* info, const 
 extern "C" void nedf_trainer_destroy(NedfTrainer* t) {
   if (!t) return;
   cudaSetDevice(t->device);
-  if (t->blas) cublasDestroy(t->blas);
-  for (auto* b : {&t->params, &t->grads, &t->m, &t->v, &t->feats, &t->xs, &t->a1, &t->h1, &t->a2, &t->la65, &t->lf,
+  for (auto* b : {&t->ws, &t->params, &t->grads, &t->m, &t->v, &t->feats, &t->xs, &t->a1, &t->h1, &t->a2, &t->la65, &t->lf,
                   &t->gx, &t->gtmp, &t->g2, &t->valid})
     b->release();
   t->o.release(); t->d.release(); t->sums.release(); t->hit.release(); t->tc.release(); t->tf.release();
@@ -408,7 +426,7 @@ extern "C" int nedf_trainer_set_batch(NedfTrainer* t, const float* feats_host, c
 extern "C" int nedf_trainer_loss_and_grads(NedfTrainer* t, double* losses_host, void* stream) {
   if (!t || !losses_host || t->n <= 0) return tfail(NEDF_ERR_INVALID, "no batch");
   cudaStream_t st = (cudaStream_t)stream;
-  BTRY(cublasSetStream(t->blas, st));
+  TTRY(cudaSetDevice(t->device));
   const Dims& D = t->dm;
   const int B = t->n, F = D.F, NB = D.NB;
   float* P = t->params.p;
@@ -419,18 +437,18 @@ extern "C" int nedf_trainer_loss_and_grads(NedfTrainer* t, double* losses_host, 
   auto A2 = [&](int i) { return t->a2.p + (size_t)i * B * F; };
   const int nb = blocks((int64_t)B * F);
   // ---- forward (nn.py:115-135)
-  BTRY(gemm_xwT(t->blas, t->feats.p, P + D.off_head_w, X(0), B, F, kDin));
+  BTRY(gemm_xwT(t, t->feats.p, P + D.off_head_w, X(0), B, F, kDin, st));
   bias_kernel<<<nb, 256, 0, st>>>(X(0), P + D.off_head_b, B, F);
   for (int i = 0; i < NB; ++i) {
-    BTRY(gemm_xwT(t->blas, X(i), P + D.off_w1(i), A1(i), B, F, F));
+    BTRY(gemm_xwT(t, X(i), P + D.off_w1(i), A1(i), B, F, F, st));
     bias_relu_kernel<<<nb, 256, 0, st>>>(A1(i), P + D.off_b1(i), H1(i), B, F);
-    BTRY(gemm_xwT(t->blas, H1(i), P + D.off_w2(i), A2(i), B, F, F));
+    BTRY(gemm_xwT(t, H1(i), P + D.off_w2(i), A2(i), B, F, F, st));
     residual_kernel<<<nb, 256, 0, st>>>(A2(i), P + D.off_b2(i), X(i), X(i + 1), B, F);
   }
   float* feat = X(NB);
-  BTRY(gemm_xwT(t->blas, feat, P + D.off_tail_a_w, t->la65.p, B, kNa, F));
+  BTRY(gemm_xwT(t, feat, P + D.off_tail_a_w, t->la65.p, B, kNa, F, st));
   bias_kernel<<<blocks((int64_t)B * kNa), 256, 0, st>>>(t->la65.p, P + D.off_tail_a_b, B, kNa);
-  BTRY(gemm_xwT(t->blas, feat, P + D.off_tail_b_w, t->lf.p, B, kNf, F));
+  BTRY(gemm_xwT(t, feat, P + D.off_tail_b_w, t->lf.p, B, kNf, F, st));
   bias_kernel<<<blocks((int64_t)B * kNf), 256, 0, st>>>(t->lf.p, P + D.off_tail_b_b, B, kNf);
   // ---- loss (the row-mask count needs the number of rows with a hit)
   std::vector<float> valid_h(B);
@@ -446,25 +464,25 @@ extern "C" int nedf_trainer_loss_and_grads(NedfTrainer* t, double* losses_host, 
                                                                 inv_c, inv_f, inv_a, t->sums.p);
   TTRY(cudaGetLastError());
   // ---- backward (nn.py:138-167); la65 / lf now hold g_a (with 0.1 alpha) and g_f
-  BTRY(gemm_gTx(t->blas, t->la65.p, feat, G + D.off_tail_a_w, B, kNa, F));
-  colsum_kernel<<<(kNa + 31) / 32, 256, 0, st>>>(t->la65.p, B, kNa, G + D.off_tail_a_b);
-  BTRY(gemm_gTx(t->blas, t->lf.p, feat, G + D.off_tail_b_w, B, kNf, F));
-  colsum_kernel<<<(kNf + 31) / 32, 256, 0, st>>>(t->lf.p, B, kNf, G + D.off_tail_b_b);
-  BTRY(gemm_gW(t->blas, t->la65.p, P + D.off_tail_a_w, t->gx.p, B, kNa, F, 0.f));
-  BTRY(gemm_gW(t->blas, t->lf.p, P + D.off_tail_b_w, t->gx.p, B, kNf, F, 1.f));
+  BTRY(gemm_gTx(t, t->la65.p, feat, G + D.off_tail_a_w, B, kNa, F, st));
+  TTRY(colsum(t, t->la65.p, B, kNa, G + D.off_tail_a_b, st));
+  BTRY(gemm_gTx(t, t->lf.p, feat, G + D.off_tail_b_w, B, kNf, F, st));
+  TTRY(colsum(t, t->lf.p, B, kNf, G + D.off_tail_b_b, st));
+  BTRY(gemm_gW(t, t->la65.p, P + D.off_tail_a_w, t->gx.p, B, kNa, F, 0.f, st));
+  BTRY(gemm_gW(t, t->lf.p, P + D.off_tail_b_w, t->gx.p, B, kNf, F, 1.f, st));
   const int ncs = (F + 31) / 32;
   for (int i = NB - 1; i >= 0; --i) {
     relu_mask_kernel<<<nb, 256, 0, st>>>(A2(i), t->gx.p, t->g2.p, (int64_t)B * F);          // g_a2
-    BTRY(gemm_gTx(t->blas, t->g2.p, H1(i), G + D.off_w2(i), B, F, F));
-    colsum_kernel<<<ncs, 256, 0, st>>>(t->g2.p, B, F, G + D.off_b2(i));
-    BTRY(gemm_gW(t->blas, t->g2.p, P + D.off_w2(i), t->gtmp.p, B, F, F, 0.f));              // g_h1
+    BTRY(gemm_gTx(t, t->g2.p, H1(i), G + D.off_w2(i), B, F, F, st));
+    TTRY(colsum(t, t->g2.p, B, F, G + D.off_b2(i), st));
+    BTRY(gemm_gW(t, t->g2.p, P + D.off_w2(i), t->gtmp.p, B, F, F, 0.f, st));              // g_h1
     relu_mask_kernel<<<nb, 256, 0, st>>>(A1(i), t->gtmp.p, t->g2.p, (int64_t)B * F);        // g_a1
-    BTRY(gemm_gTx(t->blas, t->g2.p, X(i), G + D.off_w1(i), B, F, F));
-    colsum_kernel<<<ncs, 256, 0, st>>>(t->g2.p, B, F, G + D.off_b1(i));
-    BTRY(gemm_gW(t->blas, t->g2.p, P + D.off_w1(i), t->gx.p, B, F, F, 1.f));                // g_x += g_a1 W1
+    BTRY(gemm_gTx(t, t->g2.p, X(i), G + D.off_w1(i), B, F, F, st));
+    TTRY(colsum(t, t->g2.p, B, F, G + D.off_b1(i), st));
+    BTRY(gemm_gW(t, t->g2.p, P + D.off_w1(i), t->gx.p, B, F, F, 1.f, st));                // g_x += g_a1 W1
   }
-  BTRY(gemm_gTx(t->blas, t->gx.p, t->feats.p, G + D.off_head_w, B, F, kDin));
-  colsum_kernel<<<ncs, 256, 0, st>>>(t->gx.p, B, F, G + D.off_head_b);
+  BTRY(gemm_gTx(t, t->gx.p, t->feats.p, G + D.off_head_w, B, F, kDin, st));
+  TTRY(colsum(t, t->gx.p, B, F, G + D.off_head_b, st));
   TTRY(cudaGetLastError());
   double s[4];
   TTRY(cudaMemcpyAsync(s, t->sums.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));

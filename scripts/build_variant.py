@@ -21,6 +21,6 @@ r = subprocess.run([B.nvcc(), *B.ARCH, *B.NVCC_FLAGS, *defs, "-c", str(src), "-o
 if r.returncode != 0:
     sys.exit(r.stderr)
 objs = [obj if o.stem == src.stem else o for o in sorted(B.OBJDIR.glob("*.o"))]
-subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-o", str(out_dir / f"{name}.so"), *map(str, objs), "-lcudart", "-lcublas"],
+subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-o", str(out_dir / f"{name}.so"), *map(str, objs), "-lcudart"],
                check=True)
 print(out_dir / f"{name}.so")
