@@ -27,6 +27,16 @@ int nedf_diag_umma(const void* a_dev, const void* b_dev, float* d_dev, int k, in
 int nedf_diag_umma32(const float* a_dev, const float* b_dev, float* draw_dev, int m, int n, int k, int bf16,
                      void* stream);
 
+/* The trainer's fp32-accurate split-tf32 tcgen05 GEMM: C[m][n] = op(A)[m][k] op(B)[n][k]^T
+ * (+ beta C); ta / tb = 1: that operand is stored transposed (A[k][m], B[k][n]); ws: optional
+ * split-K workspace of ws_floats floats. */
+int nedf_diag_gemm(const float* a, int lda, int ta, const float* b, int ldb, int tb, float* c, int ldc, int m, int n,
+                   int k, float beta, float* ws, int64_t ws_floats, void* stream);
+
+/* clock64 stamps of the GEMM's CTA (0, 0, 0): [0] start, [1] set up, [2 + c] chunk c ready
+ * (c < 8), [10] accumulators complete, [11] stored; enable >= 0 switches tracing. */
+int nedf_diag_gemm_trace(int enable, unsigned long long* out);
+
 /* Raw network logits for local rays (rows that miss the box are left
  * untouched): precision NEDF_PREC_TENSOR (tcgen05 kernel), NEDF_PREC_FP32, or
  * 16 + NEDF_GUARD_* (only that near-tie guard kernel, on every ray). */

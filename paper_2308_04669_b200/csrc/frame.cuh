@@ -90,9 +90,25 @@ cudaError_t launch_guard_tc(const GroupTable& gt, const ListSet& ls, const RayJo
 cudaError_t guard_tc_pack(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
                           void** dev);
 // fp32-accurate split-tf32 tcgen05 GEMM (train_gemm.cu): C[M][N] (+)= op(A)[M][K] op(B)[N][K]^T,
-// ta / tb: operand stored transposed; ws (optional) for split K over the CTAs
+// ta / tb: operand stored transposed; ws (optional) for split K over the CTAs; a fused
+// elementwise epilogue on v = acc (+ beta C), all arrays [M][ldc]:
+enum GemmEpiMode : int {
+  GEMM_EPI_NONE = 0,        // C = v
+  GEMM_EPI_BIAS = 1,        // C = v + bias[col]
+  GEMM_EPI_BIAS_RELU = 2,   // C = a = v + bias[col]; aux = relu(a)
+  GEMM_EPI_RESIDUAL = 3,    // C = a = v + bias[col]; aux = in + relu(a)
+  GEMM_EPI_MASK = 4,        // C = in > 0 ? v : 0
+  GEMM_EPI_MASK_AUX = 5     // C = v; aux = in > 0 ? v : 0
+};
+struct GemmEpi {
+  int mode = GEMM_EPI_NONE;
+  const float* bias = nullptr;
+  const float* in = nullptr;
+  float* aux = nullptr;
+};
 cudaError_t gemm_tf32x3(const float* A, int lda, int ta, const float* B, int ldb, int tb, float* C, int ldc, int M,
-                        int N, int K, float beta, float* ws, size_t ws_floats, int n_sms, cudaStream_t st);
+                        int N, int K, float beta, float* ws, size_t ws_floats, int n_sms, cudaStream_t st,
+                        const GemmEpi& epi = GemmEpi());
 // copy the 8 frame counters to mapped host memory and clear them (nedf_read_stats)
 cudaError_t launch_stats_export(unsigned long long* stats, unsigned long long* host_mapped, cudaStream_t st);
 bool tc_available();

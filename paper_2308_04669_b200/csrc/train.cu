@@ -140,33 +140,6 @@ __global__ void targets_kernel(const NedfField* fields, int root, double t_max, 
   }
 }
 
-// ---- forward epilogues ------------------------------------------------------------------
-__global__ void bias_kernel(float* __restrict__ y, const float* __restrict__ b, int rows, int cols) {
-  const int64_t n = (int64_t)rows * cols;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] += b[i % cols];
-}
-// a1 += b1 (pre-activation kept); h1 = relu(a1)
-__global__ void bias_relu_kernel(float* __restrict__ a, const float* __restrict__ b, float* __restrict__ h, int rows,
-                                 int cols) {
-  const int64_t n = (int64_t)rows * cols;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = a[i] + b[i % cols];
-    a[i] = v;
-    h[i] = fmaxf(v, 0.f);
-  }
-}
-// a2 += b2; x_out = x_in + relu(a2)  (nn.py:129-131)
-__global__ void residual_kernel(float* __restrict__ a, const float* __restrict__ b, const float* __restrict__ xin,
-                                float* __restrict__ xout, int rows, int cols) {
-  const int64_t n = (int64_t)rows * cols;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = a[i] + b[i % cols];
-    a[i] = v;
-    xout[i] = xin[i] + fmaxf(v, 0.f);
-  }
-}
-
 // ---- loss (nn.py:178-196): BCE and its logit gradient, rows masked for the bin heads ------
 __device__ __forceinline__ float bce_elem(float z, float t) {
   return fmaxf(z, 0.f) - z * t + log1pf(expf(-fabsf(z)));
@@ -214,12 +187,6 @@ __global__ void loss_kernel(float* __restrict__ la65, float* __restrict__ lf, co
 }
 
 // ---- backward helpers --------------------------------------------------------------------
-// g_out = (a > 0) ? g : 0
-__global__ void relu_mask_kernel(const float* __restrict__ a, const float* __restrict__ g, float* __restrict__ out,
-                                 int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = a[i] > 0.f ? g[i] : 0.f;
-}
 // db[c] = sum_r g[r][c] in two deterministic passes: block (column block, row slice) sums its
 // slice into part[slice][c] (8 warps striding the slice's rows, then a fixed-order combine),
 // then colsum_final adds the slices in order
@@ -298,8 +265,9 @@ cudaError_t colsum(NedfTrainer* t, const float* g, int rows, int cols, float* db
 }
 
 // Y[rows][N] = X[rows][K] . W[N][K]^T  (row-major)
-cudaError_t gemm_xwT(NedfTrainer* t, const float* X, const float* W, float* Y, int rows, int N, int K, cudaStream_t st) {
-  return gemm_tf32x3(X, K, 0, W, K, 0, Y, N, rows, N, K, 0.f, nullptr, 0, t->n_sms, st);
+cudaError_t gemm_xwT(NedfTrainer* t, const float* X, const float* W, float* Y, int rows, int N, int K, cudaStream_t st,
+                     const GemmEpi& epi) {
+  return gemm_tf32x3(X, K, 0, W, K, 0, Y, N, rows, N, K, 0.f, nullptr, 0, t->n_sms, st, epi);
 }
 // dW[N][K] = G[rows][N]^T . X[rows][K]  (reduction over the batch: split K)
 cudaError_t gemm_gTx(NedfTrainer* t, const float* G, const float* X, float* dW, int rows, int N, int K, cudaStream_t st) {
@@ -307,8 +275,16 @@ cudaError_t gemm_gTx(NedfTrainer* t, const float* G, const float* X, float* dW, 
 }
 // dX[rows][K] (+)= G[rows][N] . W[N][K]
 cudaError_t gemm_gW(NedfTrainer* t, const float* G, const float* W, float* dX, int rows, int N, int K, float beta,
-                    cudaStream_t st) {
-  return gemm_tf32x3(G, N, 0, W, K, 1, dX, K, rows, K, N, beta, nullptr, 0, t->n_sms, st);
+                    cudaStream_t st, const GemmEpi& epi = GemmEpi()) {
+  return gemm_tf32x3(G, N, 0, W, K, 1, dX, K, rows, K, N, beta, nullptr, 0, t->n_sms, st, epi);
+}
+GemmEpi epi_of(int mode, const float* bias, const float* in = nullptr, float* aux = nullptr) {
+  GemmEpi e;
+  e.mode = mode;
+  e.bias = bias;
+  e.in = in;
+  e.aux = aux;
+  return e;
 }
 
 }  // namespace
@@ -435,21 +411,18 @@ extern "C" int nedf_trainer_loss_and_grads(NedfTrainer* t, double* losses_host, 
   auto A1 = [&](int i) { return t->a1.p + (size_t)i * B * F; };
   auto H1 = [&](int i) { return t->h1.p + (size_t)i * B * F; };
   auto A2 = [&](int i) { return t->a2.p + (size_t)i * B * F; };
-  const int nb = blocks((int64_t)B * F);
   // ---- forward (nn.py:115-135)
-  BTRY(gemm_xwT(t, t->feats.p, P + D.off_head_w, X(0), B, F, kDin, st));
-  bias_kernel<<<nb, 256, 0, st>>>(X(0), P + D.off_head_b, B, F);
+  // (bias, ReLU and the residual add are the GEMMs' fused epilogues)
+  BTRY(gemm_xwT(t, t->feats.p, P + D.off_head_w, X(0), B, F, kDin, st, epi_of(GEMM_EPI_BIAS, P + D.off_head_b)));
   for (int i = 0; i < NB; ++i) {
-    BTRY(gemm_xwT(t, X(i), P + D.off_w1(i), A1(i), B, F, F, st));
-    bias_relu_kernel<<<nb, 256, 0, st>>>(A1(i), P + D.off_b1(i), H1(i), B, F);
-    BTRY(gemm_xwT(t, H1(i), P + D.off_w2(i), A2(i), B, F, F, st));
-    residual_kernel<<<nb, 256, 0, st>>>(A2(i), P + D.off_b2(i), X(i), X(i + 1), B, F);
+    BTRY(gemm_xwT(t, X(i), P + D.off_w1(i), A1(i), B, F, F, st,
+                  epi_of(GEMM_EPI_BIAS_RELU, P + D.off_b1(i), nullptr, H1(i))));
+    BTRY(gemm_xwT(t, H1(i), P + D.off_w2(i), A2(i), B, F, F, st,
+                  epi_of(GEMM_EPI_RESIDUAL, P + D.off_b2(i), X(i), X(i + 1))));
   }
   float* feat = X(NB);
-  BTRY(gemm_xwT(t, feat, P + D.off_tail_a_w, t->la65.p, B, kNa, F, st));
-  bias_kernel<<<blocks((int64_t)B * kNa), 256, 0, st>>>(t->la65.p, P + D.off_tail_a_b, B, kNa);
-  BTRY(gemm_xwT(t, feat, P + D.off_tail_b_w, t->lf.p, B, kNf, F, st));
-  bias_kernel<<<blocks((int64_t)B * kNf), 256, 0, st>>>(t->lf.p, P + D.off_tail_b_b, B, kNf);
+  BTRY(gemm_xwT(t, feat, P + D.off_tail_a_w, t->la65.p, B, kNa, F, st, epi_of(GEMM_EPI_BIAS, P + D.off_tail_a_b)));
+  BTRY(gemm_xwT(t, feat, P + D.off_tail_b_w, t->lf.p, B, kNf, F, st, epi_of(GEMM_EPI_BIAS, P + D.off_tail_b_b)));
   // ---- loss (the row-mask count needs the number of rows with a hit)
   std::vector<float> valid_h(B);
   TTRY(cudaMemcpyAsync(valid_h.data(), t->valid.p, B * sizeof(float), cudaMemcpyDeviceToHost, st));
@@ -469,17 +442,19 @@ extern "C" int nedf_trainer_loss_and_grads(NedfTrainer* t, double* losses_host, 
   BTRY(gemm_gTx(t, t->lf.p, feat, G + D.off_tail_b_w, B, kNf, F, st));
   TTRY(colsum(t, t->lf.p, B, kNf, G + D.off_tail_b_b, st));
   BTRY(gemm_gW(t, t->la65.p, P + D.off_tail_a_w, t->gx.p, B, kNa, F, 0.f, st));
-  BTRY(gemm_gW(t, t->lf.p, P + D.off_tail_b_w, t->gx.p, B, kNf, F, 1.f, st));
-  const int ncs = (F + 31) / 32;
+  // g_x; with blocks, also g_a2 = (a2 > 0) g_x of the last block (fused epilogue)
+  BTRY(gemm_gW(t, t->lf.p, P + D.off_tail_b_w, t->gx.p, B, kNf, F, 1.f, st,
+               NB > 0 ? epi_of(GEMM_EPI_MASK_AUX, nullptr, A2(NB - 1), t->g2.p) : GemmEpi()));
   for (int i = NB - 1; i >= 0; --i) {
-    relu_mask_kernel<<<nb, 256, 0, st>>>(A2(i), t->gx.p, t->g2.p, (int64_t)B * F);          // g_a2
     BTRY(gemm_gTx(t, t->g2.p, H1(i), G + D.off_w2(i), B, F, F, st));
     TTRY(colsum(t, t->g2.p, B, F, G + D.off_b2(i), st));
-    BTRY(gemm_gW(t, t->g2.p, P + D.off_w2(i), t->gtmp.p, B, F, F, 0.f, st));              // g_h1
-    relu_mask_kernel<<<nb, 256, 0, st>>>(A1(i), t->gtmp.p, t->g2.p, (int64_t)B * F);        // g_a1
-    BTRY(gemm_gTx(t, t->g2.p, X(i), G + D.off_w1(i), B, F, F, st));
-    TTRY(colsum(t, t->g2.p, B, F, G + D.off_b1(i), st));
-    BTRY(gemm_gW(t, t->g2.p, P + D.off_w1(i), t->gx.p, B, F, F, 1.f, st));                // g_x += g_a1 W1
+    // g_a1 = (a1 > 0) g_h1, g_h1 = g_a2 W2
+    BTRY(gemm_gW(t, t->g2.p, P + D.off_w2(i), t->gtmp.p, B, F, F, 0.f, st, epi_of(GEMM_EPI_MASK, nullptr, A1(i))));
+    BTRY(gemm_gTx(t, t->gtmp.p, X(i), G + D.off_w1(i), B, F, F, st));
+    TTRY(colsum(t, t->gtmp.p, B, F, G + D.off_b1(i), st));
+    // g_x += g_a1 W1; g_a2 of block i - 1 = (a2 > 0) g_x
+    BTRY(gemm_gW(t, t->gtmp.p, P + D.off_w1(i), t->gx.p, B, F, F, 1.f, st,
+                 i > 0 ? epi_of(GEMM_EPI_MASK_AUX, nullptr, A2(i - 1), t->g2.p) : GemmEpi()));
   }
   BTRY(gemm_gTx(t, t->gx.p, t->feats.p, G + D.off_head_w, B, F, kDin, st));
   TTRY(colsum(t, t->gx.p, B, F, G + D.off_head_b, st));

@@ -6,7 +6,7 @@
 // is split like the near-tie guard's (guard_tc.cu): x = x_hi + x_lo with x_hi =
 // x truncated to tf32 (what kind::tf32 reads from the raw fp32 value) and x_lo
 // the remainder rounded to tf32; three MMAs per k-step accumulate
-//   A_hi B_hi              into two alternating "main" accumulators (by K chunk:
+//   A_hi B_hi              into 1-7 rotating "main" accumulators (by K chunk:
 //                          fewer additions per accumulator keep the tensor
 //                          core's accumulation rounding at the fp32 level)
 //   A_hi B_lo + A_lo B_hi  into a "cross" accumulator
@@ -40,6 +40,8 @@ constexpr uint32_t kStage = 2 * kATile + 2 * kBTile;   // A_raw, A_lo, B_raw, B_
 constexpr int kStages = 4;                      // 192 KB ring
 static_assert(kStages * kStage >= kBM * (kBN + 1) * 4, "epilogue tile fits the ring");
 constexpr int kLoadWarps = 8;
+constexpr int kMaxMains = 7;                    // main accumulators (rotating by K chunk) + 1 cross: 512 TMEM columns
+constexpr int kChunksPerMain = 16;              // at most ~64 MMAs accumulate into one
 constexpr int kThreads = 32 * kLoadWarps;       // loader threads (+ one MMA warp)
 
 struct GemmArgs {
@@ -51,7 +53,21 @@ struct GemmArgs {
   int ta, tb;                // 1: op(A)[m][k] = A[k * lda + m] (else A[m * lda + k]); same for B
   float beta;                // C = acc + beta * C (no split)
   int k_per_split;           // multiple of kBK
+  GemmEpi epi;               // fused elementwise epilogue
 };
+
+// the fused epilogue on one output element (row r, column c) with v = acc (+ beta C)
+__device__ __forceinline__ void epi_store(const GemmEpi& e, float* C, int ldc, int r, int c, float v) {
+  const size_t i = (size_t)r * ldc + c;
+  switch (e.mode) {
+    case GEMM_EPI_BIAS: C[i] = v + e.bias[c]; break;
+    case GEMM_EPI_BIAS_RELU: { const float a = v + e.bias[c]; C[i] = a; e.aux[i] = fmaxf(a, 0.f); break; }
+    case GEMM_EPI_RESIDUAL: { const float a = v + e.bias[c]; C[i] = a; e.aux[i] = e.in[i] + fmaxf(a, 0.f); break; }
+    case GEMM_EPI_MASK: C[i] = e.in[i] > 0.f ? v : 0.f; break;
+    case GEMM_EPI_MASK_AUX: C[i] = v; e.aux[i] = e.in[i] > 0.f ? v : 0.f; break;
+    default: C[i] = v;
+  }
+}
 
 __device__ __forceinline__ float tf32_lo(float x) {
   const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
@@ -129,6 +145,66 @@ struct Chunk {
 
 }  // namespace
 
+// The output tile (in shared memory, [kBM][kBN + 1]) to C / the split-K workspace with the
+// fused epilogue MODE (-1: raw partial), 4 consecutive columns of a row per item: float4
+// loads / stores when the run is whole and aligned, scalar otherwise.
+template <int MODE>
+__device__ __forceinline__ void store_tile(const GemmArgs& g, const float* tile, int m0, int n0, int split) {
+  constexpr int kLd = kBN + 1, kNT = kThreads + 32;
+  constexpr bool kIn = MODE == GEMM_EPI_RESIDUAL || MODE == GEMM_EPI_MASK || MODE == GEMM_EPI_MASK_AUX;
+  constexpr bool kBias = MODE == GEMM_EPI_BIAS || MODE == GEMM_EPI_BIAS_RELU || MODE == GEMM_EPI_RESIDUAL;
+  constexpr bool kAux = MODE == GEMM_EPI_BIAS_RELU || MODE == GEMM_EPI_RESIDUAL || MODE == GEMM_EPI_MASK_AUX;
+  const GemmEpi& ep = g.epi;
+  float* out = g.C + (size_t)split * ((size_t)g.M * g.ldc);
+  const bool beta = MODE >= 0 && g.beta != 0.f;
+  auto f = [&](float x, float cold, float xin, float bb, float& aux) {
+    if (beta) x += g.beta * cold;
+    if (MODE == GEMM_EPI_BIAS) return x + bb;
+    if (MODE == GEMM_EPI_BIAS_RELU) { const float a = x + bb; aux = fmaxf(a, 0.f); return a; }
+    if (MODE == GEMM_EPI_RESIDUAL) { const float a = x + bb; aux = xin + fmaxf(a, 0.f); return a; }
+    if (MODE == GEMM_EPI_MASK) return xin > 0.f ? x : 0.f;
+    if (MODE == GEMM_EPI_MASK_AUX) { aux = xin > 0.f ? x : 0.f; return x; }
+    return x;
+  };
+  const bool vec_ok = (g.ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(out) | (kIn ? reinterpret_cast<uintptr_t>(ep.in) : 0) |
+                                            (kAux ? reinterpret_cast<uintptr_t>(ep.aux) : 0)) & 15) == 0 &&
+                      (!kBias || (reinterpret_cast<uintptr_t>(ep.bias) & 15) == 0);
+  for (int e = threadIdx.x; e < kBM * kBN / 4; e += kNT) {
+    const int r = e / (kBN / 4), c4 = (e % (kBN / 4)) * 4;
+    const int gr = m0 + r, gc = n0 + c4;
+    if (gr >= g.M || gc >= g.N) continue;
+    const size_t at = (size_t)gr * g.ldc + gc;
+    const float* t = tile + r * kLd + c4;
+    if (vec_ok && gc + 4 <= g.N) {
+      float4 cold = make_float4(0.f, 0.f, 0.f, 0.f), xin = cold, bb = cold, aux = cold;
+      if (beta) cold = *reinterpret_cast<const float4*>(out + at);
+      if (kIn) xin = *reinterpret_cast<const float4*>(ep.in + at);
+      if (kBias) bb = *reinterpret_cast<const float4*>(ep.bias + gc);
+      float4 o;
+      o.x = f(t[0], cold.x, xin.x, bb.x, aux.x);
+      o.y = f(t[1], cold.y, xin.y, bb.y, aux.y);
+      o.z = f(t[2], cold.z, xin.z, bb.z, aux.z);
+      o.w = f(t[3], cold.w, xin.w, bb.w, aux.w);
+      *reinterpret_cast<float4*>(out + at) = o;
+      if (kAux) *reinterpret_cast<float4*>(ep.aux + at) = aux;
+    } else {
+      for (int j = 0; j < 4 && gc + j < g.N; ++j) {
+        float aux = 0.f;
+        const float o = f(t[j], beta ? out[at + j] : 0.f, kIn ? ep.in[at + j] : 0.f, kBias ? ep.bias[gc + j] : 0.f, aux);
+        out[at + j] = o;
+        if (kAux) ep.aux[at + j] = aux;
+      }
+    }
+  }
+}
+
+__device__ unsigned long long g_gemm_trace[16];
+__device__ int g_gemm_trace_on;
+#define GEMM_TRACE(i)                                                                                 \
+  do {                                                                                                \
+    if (g_gemm_trace_on && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) g_gemm_trace[i] = clock64(); \
+  } while (0)
+
 __global__ void __launch_bounds__(kThreads + 32, 1) gemm_tf32x3_kernel(GemmArgs g) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -139,6 +215,8 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemm_tf32x3_kernel(GemmArgs 
   const int k_begin = split * g.k_per_split;
   const int k_end = min(g.K, k_begin + g.k_per_split);
   const int n_chunks = max(0, (k_end - k_begin + kBK - 1) / kBK);
+  if (tid == 0) GEMM_TRACE(0);
+  const int mains = max(1, min(kMaxMains, (n_chunks + kChunksPerMain - 1) / kChunksPerMain));
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
       tc::mbar_init(&full_bar[i], kLoadWarps);
@@ -147,28 +225,42 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemm_tf32x3_kernel(GemmArgs 
     tc::mbar_init(&done_bar, 1);
     tc::mbar_fence_init();
   }
-  if (warp == 0) tc::tmem_alloc<256>(&tmem_base_s);      // main 0 / main 1 / cross: 3 x 64 columns
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base_s);      // kMains main accumulators + cross: 8 x 64 columns
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = tmem_base_s;
+  if (tid == 0) GEMM_TRACE(1);
   auto stage = [&](int s) { return smem + (size_t)s * kStage; };
   if (warp < kLoadWarps) {
-    // ---- loaders: chunk c -> registers -> (wait for the slot) -> raw / lo tiles, kStages ahead
-    Chunk<kBM> ra;
-    Chunk<kBN> rb;
-    for (int c = 0; c < n_chunks; ++c) {
-      const int s = c % kStages;
+    // ---- loaders: chunk c -> registers -> (wait for the slot) -> raw / lo tiles, kStages ahead;
+    // two register buffers, so chunk c + 2's loads are in flight while chunk c is stored
+    Chunk<kBM> ra[2];
+    Chunk<kBN> rb[2];
+    auto fetch = [&](int c, Chunk<kBM>& a, Chunk<kBN>& b) {
       const int k0 = k_begin + c * kBK;
-      ra.fetch(g.A, g.lda, g.ta, m0, g.M, k0, k_end);
-      rb.fetch(g.B, g.ldb, g.tb, n0, g.N, k0, k_end);
+      a.fetch(g.A, g.lda, g.ta, m0, g.M, k0, k_end);
+      b.fetch(g.B, g.ldb, g.tb, n0, g.N, k0, k_end);
+    };
+    auto store = [&](int c, const Chunk<kBM>& a, const Chunk<kBN>& b) {
+      const int s = c % kStages;
       if (c >= kStages) tc::mbar_wait(&empty_bar[s], ((c / kStages) - 1) & 1);
       unsigned char* st = stage(s);
-      ra.put(g.ta, st, st + kATile);
-      rb.put(g.tb, st + 2 * kATile, st + 2 * kATile + kBTile);
+      a.put(g.ta, st, st + kATile);
+      b.put(g.tb, st + 2 * kATile, st + 2 * kATile + kBTile);
       tc::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&full_bar[s]);
+    };
+    if (n_chunks > 0) fetch(0, ra[0], rb[0]);
+    if (n_chunks > 1) fetch(1, ra[1], rb[1]);
+    for (int c = 0; c < n_chunks; c += 2) {
+      store(c, ra[0], rb[0]);
+      if (c + 2 < n_chunks) fetch(c + 2, ra[0], rb[0]);
+      if (c + 1 < n_chunks) {
+        store(c + 1, ra[1], rb[1]);
+        if (c + 3 < n_chunks) fetch(c + 3, ra[1], rb[1]);
+      }
     }
   } else {
     // ---- MMA issuer (warp kLoadWarps)
@@ -177,15 +269,16 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemm_tf32x3_kernel(GemmArgs 
       const int s = c % kStages;
       tc::mbar_wait(&full_bar[s], (c / kStages) & 1);
       tc::tc_fence_after();
+      if (lane == 0 && c < 8) GEMM_TRACE(2 + c);
       if (tc::elect_one()) {
         const uint32_t sa = tc::smem_u32(stage(s));
         const uint64_t a_raw = tc::sw128_desc(sa), a_lo = tc::sw128_desc(sa + kATile);
         const uint64_t b_raw = tc::sw128_desc(sa + 2 * kATile), b_lo = tc::sw128_desc(sa + 2 * kATile + kBTile);
-        const uint32_t d_main = tbase + 64 * (c & 1), d_cross = tbase + 128;
+        const uint32_t d_main = tbase + 64 * (1 + c % mains), d_cross = tbase;
 #pragma unroll
         for (int ks = 0; ks < kBK / 8; ++ks) {
           const uint32_t o = (ks * 32) >> 4;
-          tc::mma_ss_tf32(d_main, a_raw + o, b_raw + o, idesc, (c < 2 && ks == 0) ? 0u : 1u);
+          tc::mma_ss_tf32(d_main, a_raw + o, b_raw + o, idesc, (c < mains && ks == 0) ? 0u : 1u);
           tc::mma_ss_tf32(d_cross, a_raw + o, b_lo + o, idesc, (c == 0 && ks == 0) ? 0u : 1u);
           tc::mma_ss_tf32(d_cross, a_lo + o, b_raw + o, idesc, 1u);
         }
@@ -197,6 +290,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemm_tf32x3_kernel(GemmArgs 
   }
   if (n_chunks > 0) tc::mbar_wait(&done_bar, 0);
   tc::tc_fence_after();
+  if (tid == 0) GEMM_TRACE(10);
   __syncthreads();
   // ---- epilogue: TMEM -> registers (warps 0-3, thread = row) -> a padded shared tile (the
   // ring is free now) -> coalesced row stores by all loader warps
@@ -205,53 +299,73 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemm_tf32x3_kernel(GemmArgs 
   if (warp < 4) {
     const int r = 32 * warp + lane;
     const uint32_t lb = (uint32_t)(32 * warp) << 16;
+    const int used = min(n_chunks, mains);                    // main accumulators written
     for (int j0 = 0; j0 < kBN; j0 += 16) {
-      uint32_t r0[16], r1[16], rc[16];
-      tc::tmem_ld16(tbase + lb + j0, r0);
-      tc::tmem_ld16(tbase + lb + 64 + j0, r1);
-      tc::tmem_ld16(tbase + lb + 128 + j0, rc);
-      tc::tmem_ld_wait();
+      // the cross accumulator and up to three mains per wait
+      float acc[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        tile[r * kLd + j0 + j] = n_chunks == 0 ? 0.f
-                                 : (__uint_as_float(r0[j]) + (n_chunks > 1 ? __uint_as_float(r1[j]) : 0.f)) +
-                                       __uint_as_float(rc[j]);
+      for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+      for (int i0 = 0; i0 <= used; i0 += 4) {
+        uint32_t rv[4][16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i0 + q <= used) tc::tmem_ld16(tbase + lb + 64 * (i0 + q) + j0, rv[q]);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i0 + q <= used && n_chunks > 0) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(rv[q][j]);
+          }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) tile[r * kLd + j0 + j] = acc[j];
     }
+    if (tid == 0) GEMM_TRACE(12);
   }
   __syncthreads();
-  float* out = g.C + (size_t)split * ((size_t)g.M * g.ldc);
-  const bool use_beta = gridDim.z == 1 && g.beta != 0.f;
-  for (int e = tid; e < kBM * kBN; e += kThreads + 32) {
-    const int r = e / kBN, col = e % kBN;
-    const int gr = m0 + r, gc = n0 + col;
-    if (gr < g.M && gc < g.N) {
-      float* dst = out + (size_t)gr * g.ldc + gc;
-      const float v = tile[r * kLd + col];
-      *dst = use_beta ? v + g.beta * *dst : v;
-    }
+  if (tid == 0) GEMM_TRACE(13);
+  const GemmEpi& ep = g.epi;
+  switch (gridDim.z > 1 ? -1 : ep.mode) {
+    case -1: store_tile<-1>(g, tile, m0, n0, split); break;     // split-K partial: the reduce kernel finishes
+    case GEMM_EPI_BIAS: store_tile<GEMM_EPI_BIAS>(g, tile, m0, n0, split); break;
+    case GEMM_EPI_BIAS_RELU: store_tile<GEMM_EPI_BIAS_RELU>(g, tile, m0, n0, split); break;
+    case GEMM_EPI_RESIDUAL: store_tile<GEMM_EPI_RESIDUAL>(g, tile, m0, n0, split); break;
+    case GEMM_EPI_MASK: store_tile<GEMM_EPI_MASK>(g, tile, m0, n0, split); break;
+    case GEMM_EPI_MASK_AUX: store_tile<GEMM_EPI_MASK_AUX>(g, tile, m0, n0, split); break;
+    default: store_tile<GEMM_EPI_NONE>(g, tile, m0, n0, split);
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<256>(tbase);
+  if (tid == 0) GEMM_TRACE(11);
+  if (warp == 0) tc::tmem_dealloc<512>(tbase);
+}
+
+extern "C" int nedf_diag_gemm_trace(int enable, unsigned long long* out) {
+  if (enable >= 0 && cudaMemcpyToSymbol(g_gemm_trace_on, &enable, sizeof(int)) != cudaSuccess) return NEDF_ERR_CUDA;
+  if (out && cudaMemcpyFromSymbol(out, g_gemm_trace, 16 * sizeof(unsigned long long)) != cudaSuccess)
+    return NEDF_ERR_CUDA;
+  return NEDF_OK;
 }
 
 // C[m][n] = sum over splits of ws[s][m][n] (+ beta C), in split order
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, float* __restrict__ C, int M, int N, int ldc,
-                                     int splits, float beta) {
+                                     int splits, float beta, GemmEpi epi) {
   const int64_t total = (int64_t)M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int m = (int)(i / N), n = (int)(i % N);
     float s = 0.f;
     for (int k = 0; k < splits; ++k) s += ws[((size_t)k * M + m) * ldc + n];
-    float* dst = C + (size_t)m * ldc + n;
-    *dst = beta != 0.f ? s + beta * *dst : s;
+    if (beta != 0.f) s += beta * C[(size_t)m * ldc + n];
+    epi_store(epi, C, ldc, m, n, s);
   }
 }
 
 // C[M][N] (+)= op(A) op(B)^T.  ws: workspace of at least ws_floats floats for split K (may be
 // NULL: no split).
 cudaError_t gemm_tf32x3(const float* A, int lda, int ta, const float* B, int ldb, int tb, float* C, int ldc, int M,
-                        int N, int K, float beta, float* ws, size_t ws_floats, int n_sms, cudaStream_t st) {
+                        int N, int K, float beta, float* ws, size_t ws_floats, int n_sms, cudaStream_t st,
+                        const GemmEpi& epi) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   static bool configured[kMaxDevices] = {};
   const size_t smem = kStages * kStage + 1024;
@@ -278,14 +392,29 @@ cudaError_t gemm_tf32x3(const float* A, int lda, int ta, const float* B, int ldb
   g.A = A; g.B = B; g.M = M; g.N = N; g.K = K; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.ta = ta; g.tb = tb;
   g.beta = beta;
   g.k_per_split = kps;
+  g.epi = epi;
   g.C = splits > 1 ? ws : C;
   gemm_tf32x3_kernel<<<dim3(gm, gn, splits), kThreads + 32, smem, st>>>(g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || splits == 1) return e;
   const int64_t total = (int64_t)M * N;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)n_sms * 8);
-  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, C, M, N, ldc, splits, beta);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, C, M, N, ldc, splits, beta, epi);
   return cudaGetLastError();
 }
 
 }  // namespace nedf
+
+// diagnostics / tests: C[M][N] = op(A) op(B)^T with the trainer's GEMM (ws may be NULL)
+extern "C" int nedf_diag_gemm(const float* a, int lda, int ta, const float* b, int ldb, int tb, float* c, int ldc,
+                              int m, int n, int k, float beta, float* ws, int64_t ws_floats, void* stream) {
+  using namespace nedf;
+  if (!a || !b || !c || m < 0 || n < 0 || k < 0) return NEDF_ERR_INVALID;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return gemm_tf32x3(a, lda, ta, b, ldb, tb, c, ldc, m, n, k, beta, ws, ws ? (size_t)ws_floats : 0, sms,
+                     (cudaStream_t)stream) == cudaSuccess
+             ? NEDF_OK
+             : NEDF_ERR_CUDA;
+}
