@@ -54,13 +54,14 @@ def parse():
 
 
 def traffic_per_launch():
-    """dram__bytes_read.sum + dram__bytes_write.sum of one network launch from the committed
-    ncu capture of the benchmarked kernel (profiles/r1_tc_kernel_ncu.json), or None."""
-    f = ROOT / "profiles" / "r1_tc_kernel_ncu.json"
-    try:
-        return json.loads(f.read_text())["dram_bytes_per_launch"]
-    except (OSError, ValueError, KeyError):
-        return None
+    """dram__bytes_read.sum + dram__bytes_write.sum of one network launch from the latest
+    committed ncu capture of the benchmarked kernel (profiles/r*_tc_kernel_ncu.json), or None."""
+    for f in sorted((ROOT / "profiles").glob("r*_tc_kernel_ncu.json"), reverse=True):
+        try:
+            return json.loads(f.read_text())["dram_bytes_per_launch"]
+        except (OSError, ValueError, KeyError):
+            continue
+    return None
 
 
 def dist_env():

@@ -7,7 +7,7 @@ the committed summaries under profiles/:
   tc_full.ncu-rep     -> <prefix>_tc_kernel_ncu.json (when the capture finished)
   bench.json / bench_ref.json / configs.jsonl -> copied
 
-usage: python scripts/summarize_profiles.py [--prefix r1] [--src gpurun_out]
+usage: python scripts/summarize_profiles.py [--prefix r2] [--src gpurun_out]
 """
 import argparse
 import csv
@@ -73,7 +73,7 @@ def rep_summary(rep: Path, kernel: str, capture: str, launch: str) -> dict:
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--prefix", default="r1")
+    ap.add_argument("--prefix", default="r2")
     ap.add_argument("--src", default=str(ROOT / "gpurun_out"))
     a = ap.parse_args()
     src, dst = Path(a.src), ROOT / "profiles"
@@ -84,13 +84,23 @@ def main():
         (dst / f"{p}_launches_config4_summary.json").write_text(json.dumps(s, indent=1) + "\n")
         shutil.copy(src / "launches.csv", dst / f"{p}_launches_config4.csv")
     base = "python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+    if (src / "train_launches.csv").exists():
+        s = launch_summary(src / "train_launches.csv", "ncu --metrics gpu__time_duration.sum --clock-control none "
+                           "-c 2000 python scripts/train_profile.py 3")
+        s["note"] = "serialised, cold-cache per-launch times; 3 paper-profile training iterations (batch 4096)"
+        (dst / f"{p}_launches_train_summary.json").write_text(json.dumps(s, indent=1) + "\n")
     for rep, kern, cap, out in [
-            ("guard_full.ncu-rep", "mlp_fp32_cluster_kernel", "--set full -k regex:mlp_fp32_cluster", "guard"),
+            ("guard_tc_kernel_full.ncu-rep", "guard_tc_kernel", "--set full -k regex:guard_tc_kernel", "guard"),
+            ("resolve_shade_kernel_full.ncu-rep", "resolve_shade_kernel", "--set full -k regex:resolve_shade_kernel",
+             "resolve_shade"),
+            ("setup_kernel_full.ncu-rep", "setup_kernel", "--set full -k regex:setup_kernel", "setup"),
+            ("gemm_full.ncu-rep", "gemm_tf32x3_kernel (trainer, forward body layer 4096 x 256 x 256)",
+             "--set full -k regex:gemm_tf32x3 -s 105 -c 1 python scripts/train_profile.py 2", "train_gemm"),
             ("tc_full.ncu-rep", "nedf_mlp_tc_kernel (cluster-multicast pair, as benchmarked)",
              "--metrics <list in scripts/gpu_round_artifacts.sh> -k regex:nedf_mlp_tc_kernel", "tc"),
             ("tc_single_full.ncu-rep", "nedf_mlp_tc_kernel (single-CTA variant)",
              "--set full -k regex:nedf_mlp_tc_kernel [--tc-kernel single]", "tc_single_full"),
-            ("setup_full.ncu-rep", "setup_kernel", "--set full -k regex:setup_kernel", "setup")]:
+            ]:
         if (src / rep).exists() and (src / rep).stat().st_size > 0:
             if out != "tc":      # full-set captures: also the section details (rules, speed-of-light, stalls)
                 det = subprocess.run(["ncu", "-i", str(src / rep), "--page", "details", "--csv"], capture_output=True,
@@ -99,8 +109,9 @@ def main():
                     name = "tc_single" if out == "tc_single_full" else out
                     (dst / f"{p}_{name}_kernel_details.csv").write_text(det)
             try:
-                s = rep_summary(src / rep, kern, f"ncu {cap} --clock-control none -s 2 -c 1 {base}",
-                                "STEP-1 launch of a config-4 frame")
+                s = rep_summary(src / rep, kern, f"ncu {cap} --clock-control none" +
+                                ("" if "train_profile" in cap else f" -s 2 -c 1 {base}"),
+                                "trainer GEMM" if out == "train_gemm" else "STEP-1 launch of a config-4 frame")
                 (dst / f"{p}_{out}_kernel_ncu.json").write_text(json.dumps(s, indent=1) + "\n")
             except (subprocess.CalledProcessError, IndexError) as e:
                 print("skip", rep, e)
