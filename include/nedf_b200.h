@@ -72,11 +72,12 @@ enum {
                                    composite); 0 = one kernel per step, as the step entry points run */
   NEDF_OPT_GUARD_KERNEL = 9     /* one of NEDF_GUARD_*: which kernel re-evaluates the near-tie rays */
 };
-/* Near-tie guard kernels (NEDF_OPT_GUARD_KERNEL); both fp32-accurate. */
+/* Near-tie guard kernels (NEDF_OPT_GUARD_KERNEL); all fp32-accurate. */
 enum {
-  NEDF_GUARD_AUTO = 0,      /* NEDF_GUARD_TCGEN05 */
-  NEDF_GUARD_TCGEN05 = 1,   /* tcgen05 tf32 + bf16 split products, 4-CTA clusters (guard_tc.cu) */
-  NEDF_GUARD_MMA_SYNC = 2   /* warp-level mma.sync 3xTF32, 4- or 8-CTA clusters (mlp_fp32c.cu) */
+  NEDF_GUARD_AUTO = 0,      /* by batch size (decided on the device): TCGEN05 when it fits one round, else PRECISE */
+  NEDF_GUARD_TCGEN05 = 1,   /* latency form: tcgen05 tf32 + fp16 split products, 16 rays per 4-CTA cluster (guard_tc.cu) */
+  NEDF_GUARD_MMA_SYNC = 2,  /* warp-level mma.sync 3xTF32, 4- or 8-CTA clusters (mlp_fp32c.cu) */
+  NEDF_GUARD_PRECISE = 3    /* throughput form: 3-product fp16 split, 128-ray tiles, one CTA per SM (mlp_precise.cu) */
 };
 
 /* Tensor-core network kernels (NEDF_OPT_TC_KERNEL). */

@@ -57,6 +57,7 @@ struct NedfModel {
   float* wT = nullptr;
   float* bias = nullptr;
   __half* wpack = nullptr;
+  __half* wpack_lo = nullptr;
   float* bias_pack = nullptr;
   float* wstream = nullptr;
   float* wcluster = nullptr;
@@ -409,6 +410,7 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
   if (F.gt.n_groups == 0) return NEDF_OK;
   if (ctx->guard_direct) {
     if (ctx->guard_direct == NEDF_GUARD_TCGEN05) LAUNCH(ctx, launch_guard_tc(F.gt, F.ls, job, out, ctx->n_sms, st));
+    else if (ctx->guard_direct == NEDF_GUARD_PRECISE) LAUNCH(ctx, launch_mlp_precise(F.gt, F.ls, job, out, ctx->n_sms, -1, st));
     else LAUNCH(ctx, launch_mlp_fp32_cluster(F.gt, F.ls, job, out, ctx->n_sms, ctx->guard_cluster ? ctx->guard_cluster : 4, st));
     return NEDF_OK;
   }
@@ -436,7 +438,14 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
       // once (vs ~33 of 4): by default they take frames with at most half a 2000 x 800 x 8-object
       // frame's (pixel, object) pairs, whose guard batch then still fits one round
       if (ctx->guard_kernel != NEDF_GUARD_MMA_SYNC && guard_tc_available()) {
-        LAUNCH(ctx, launch_guard_tc(F.gt, F.redo, job, out, ctx->n_sms, st));
+        // the batch size is only known on the device: both kernels are launched and the one that
+        // does not fit returns at once -- guard_tc (latency) for batches that fit its clusters in
+        // one round, mlp_precise (throughput: 128-ray tiles, one CTA per SM) beyond
+        const int cap = ctx->guard_kernel == NEDF_GUARD_TCGEN05 ? 1 << 30 : guard_tc_capacity(ctx->n_sms);
+        LAUNCH(ctx, launch_guard_tc(F.gt, F.redo, job, out, ctx->n_sms, st, cap));
+        if (ctx->guard_kernel == NEDF_GUARD_AUTO) LAUNCH(ctx, launch_mlp_precise(F.gt, F.redo, job, out, ctx->n_sms, cap, st));
+      } else if (ctx->guard_kernel == NEDF_GUARD_PRECISE) {
+        LAUNCH(ctx, launch_mlp_precise(F.gt, F.redo, job, out, ctx->n_sms, -1, st));
       } else {
         int cl = ctx->guard_cluster;
         if (cl == 0) cl = (int64_t)F.n_pix * F.sc.n_objs <= 6400000 ? 8 : 4;
@@ -691,7 +700,7 @@ int nedf_set_option(NedfContext* c, int key, int64_t v) {
       c->setup_exact = v != 0;
       return NEDF_OK;
     case NEDF_OPT_GUARD_KERNEL:
-      if (v != NEDF_GUARD_AUTO && v != NEDF_GUARD_TCGEN05 && v != NEDF_GUARD_MMA_SYNC)
+      if (v != NEDF_GUARD_AUTO && v != NEDF_GUARD_TCGEN05 && v != NEDF_GUARD_MMA_SYNC && v != NEDF_GUARD_PRECISE)
         return fail(NEDF_ERR_INVALID, "bad guard kernel");
       c->guard_kernel = (int)v;
       return NEDF_OK;
@@ -849,6 +858,7 @@ int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* 
     if (m->wT) cudaFree(m->wT);
     if (m->bias) cudaFree(m->bias);
     if (m->wpack) cudaFree(m->wpack);
+    if (m->wpack_lo) cudaFree(m->wpack_lo);
     if (m->bias_pack) cudaFree(m->bias_pack);
     if (m->wstream) cudaFree(m->wstream);
     if (m->wcluster) cudaFree(m->wcluster);
@@ -877,6 +887,10 @@ int nedf_model_create(NedfContext* ctx, const NedfModelInfo* info, const float* 
     if (e != cudaSuccess) { cleanup(); return fail(NEDF_ERR_CUDA, std::string("tc pack: ") + cudaGetErrorString(e)); }
     h.wpack = m->wpack;
     h.bias_pack = m->bias_pack;
+    e = tc_pack_weights(params, info->d_in, F, info->n_blocks, info->n_coarse, info->n_fine, &m->wpack_lo, nullptr,
+                        &bytes, 1);
+    if (e != cudaSuccess) { cleanup(); return fail(NEDF_ERR_CUDA, std::string("tc pack (lo): ") + cudaGetErrorString(e)); }
+    h.wpack_lo = m->wpack_lo;
     e = fp32_pack_stream(params, info->d_in, F, info->n_blocks, info->n_coarse, info->n_fine, &m->wstream);
     if (e != cudaSuccess) { cleanup(); return fail(NEDF_ERR_CUDA, std::string("fp32 pack: ") + cudaGetErrorString(e)); }
     h.wstream = m->wstream;
@@ -933,6 +947,7 @@ void nedf_model_free(NedfModel* m) {
   if (m->wT) cudaFree(m->wT);
   if (m->bias) cudaFree(m->bias);
   if (m->wpack) cudaFree(m->wpack);
+  if (m->wpack_lo) cudaFree(m->wpack_lo);
   if (m->bias_pack) cudaFree(m->bias_pack);
   if (m->wstream) cudaFree(m->wstream);
   if (m->wcluster) cudaFree(m->wcluster);
@@ -1063,7 +1078,8 @@ extern "C" int nedf_diag_ray_logits(NedfContext* ctx, const NedfModel* m, const 
   if (precision == NEDF_PREC_TENSOR && !m->host.tensor_ok) return fail(NEDF_ERR_UNSUPPORTED, "model not tensor-core shaped");
   int saved = ctx->precision;
   ctx->precision = precision == NEDF_PREC_TENSOR ? NEDF_PREC_TENSOR : NEDF_PREC_FP32;
-  if (precision == 16 + NEDF_GUARD_TCGEN05 || precision == 16 + NEDF_GUARD_MMA_SYNC) {
+  if (precision == 16 + NEDF_GUARD_TCGEN05 || precision == 16 + NEDF_GUARD_MMA_SYNC ||
+      precision == 16 + NEDF_GUARD_PRECISE) {
     if (!m->host.tensor_ok) return fail(NEDF_ERR_UNSUPPORTED, "model not tensor-core shaped");
     ctx->guard_direct = precision - 16;
   }

@@ -36,6 +36,7 @@ struct DevModel {
   const float* wT;               // fp32 [in][out] per layer (head padded to 1024 rows)
   const float* bias;             // fp32 per layer, concatenated
   const __half* wpack;           // tcgen05 operand image (see mlp_tc.cu)
+  const __half* wpack_lo;        // its low halves 4096 (w - fp16(w)) for mlp_precise.cu
   const float* bias_pack;        // tcgen05 bias image (fp32, padded to 256 per layer)
   const float* wstream;          // fp32 stream image for mlp_fp32s.cu (paper-shaped models)
   const float* wcluster;         // fp32 cluster-split images for mlp_fp32c.cu (paper-shaped models):

@@ -85,8 +85,9 @@ struct TcArgs {
 };
 // tcgen05 guard (guard_tc.cu): fp32-accurate re-evaluation of `ls` (the redo list) in 4-CTA clusters
 bool guard_tc_available();
+// max_tiles16 >= 0: return at once when the batch has more 16-ray tiles (mlp_precise takes it)
 cudaError_t launch_guard_tc(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
-                            int n_sms, cudaStream_t stream);
+                            int n_sms, cudaStream_t stream, int max_tiles16 = -1);
 cudaError_t guard_tc_pack(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
                           void** dev);
 // fp32-accurate split-tf32 tcgen05 GEMM (train_gemm.cu): C[M][N] (+)= op(A)[M][K] op(B)[N][K]^T,
@@ -114,8 +115,15 @@ cudaError_t launch_stats_export(unsigned long long* stats, unsigned long long* h
 bool tc_available();
 // csize = CTAs per cluster sharing one multicast weight stream (1, 2 or 4)
 cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, int csize, cudaStream_t stream);
-// one-time fp16 operand image of a paper-shaped model for the tensor-core kernel
+// one-time fp16 operand image of a paper-shaped model for the tensor-core kernel (part 0), or the
+// low halves 4096 (w - fp16(w)) in the same layout (part 1, mlp_precise.cu); bias_dev may be NULL
 cudaError_t tc_pack_weights(const float* params_host, int d_in, int d_feat, int n_blocks, int n_coarse, int n_fine,
-                            __half** wpack_dev, float** bias_dev, size_t* bytes);
+                            __half** wpack_dev, float** bias_dev, size_t* bytes, int part = 0);
+// fp32-accurate network for large guard batches (mlp_precise.cu): returns at once on the device
+// when the batch has at most min_tiles16 16-ray tiles (guard_tc's one round)
+cudaError_t launch_mlp_precise(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
+                               int n_sms, int min_tiles16, cudaStream_t stream);
+// co-resident 4-CTA clusters of guard_tc (its one-round capacity in 16-ray tiles)
+int guard_tc_capacity(int n_sms);
 
 }  // namespace nedf

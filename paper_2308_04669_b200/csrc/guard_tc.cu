@@ -169,7 +169,7 @@ __device__ unsigned long long g_gtrace[320];
 __device__ int g_gtrace_on;
 
 __global__ void __cluster_dims__(kGC, 1, 1) __launch_bounds__(kGThreads, 1)
-guard_tc_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
+guard_tc_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out, int max_tiles16) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   GSmem& S = *reinterpret_cast<GSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -177,6 +177,11 @@ guard_tc_kernel(GroupTable gt, ListSet ls, RayJob job, OutSpec out) {
   const int cid = blockIdx.x / kGC, n_cl = gridDim.x / kGC;
   const int ng = ls.n_groups < 64 ? ls.n_groups : 64;
   const bool feats_in = out.feats != nullptr;
+  if (max_tiles16 >= 0) {                      // large batches go to mlp_precise.cu (decided on the device)
+    int t16 = 0;
+    for (int g = 0; g < ng; ++g) t16 += (ls.count[g] + kGN - 1) / kGN;
+    if (t16 > max_tiles16) return;
+  }
 
   if (tid == 0) {
     int cum = 0;
@@ -551,9 +556,9 @@ bool guard_tc_available() {
   return major == 10 && (size_t)optin >= sizeof(GSmem) + 1024;
 }
 
-cudaError_t launch_guard_tc(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
-                            int n_sms, cudaStream_t stream) {
-  static int max_clusters_dev[kMaxDevices] = {};
+static int max_clusters_dev[kMaxDevices] = {};
+
+static cudaError_t guard_tc_setup(int n_sms) {
   int& max_clusters = max_clusters_dev[current_device()];
   const size_t smem = sizeof(GSmem) + 1024;
   if (max_clusters == 0) {
@@ -569,7 +574,20 @@ cudaError_t launch_guard_tc(const GroupTable& gt, const ListSet& ls, const RayJo
     max_clusters = n > 0 ? n : 1;
     if (getenv("NEDF_VERBOSE")) fprintf(stderr, "nedf: tcgen05 guard kernel, %d co-resident clusters\n", n);
   }
-  guard_tc_kernel<<<kGC * max_clusters, kGThreads, smem, stream>>>(gt, ls, job, out);
+  return cudaSuccess;
+}
+
+int guard_tc_capacity(int n_sms) {
+  if (guard_tc_setup(n_sms) != cudaSuccess) return 0;
+  return max_clusters_dev[current_device()];
+}
+
+cudaError_t launch_guard_tc(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
+                            int n_sms, cudaStream_t stream, int max_tiles16) {
+  cudaError_t e = guard_tc_setup(n_sms);
+  if (e != cudaSuccess) return e;
+  const int max_clusters = max_clusters_dev[current_device()];
+  guard_tc_kernel<<<kGC * max_clusters, kGThreads, sizeof(GSmem) + 1024, stream>>>(gt, ls, job, out, max_tiles16);
   return cudaGetLastError();
 }
 

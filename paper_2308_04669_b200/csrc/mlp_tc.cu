@@ -732,14 +732,16 @@ cudaError_t launch_mlp_tc(const TcArgs& a, int n_ctas, int csize, cudaStream_t s
 // rows 128s.., K chunk kc); tail rows = fine (0-127), coarse (128-191),
 // alpha (192), zero padding.  Biases: [34 layers][256] fp32, same row order.
 cudaError_t tc_pack_weights(const float* P, int d_in, int F, int n_blocks, int n_coarse, int n_fine,
-                            __half** wpack_dev, float** bias_dev, size_t* bytes) {
+                            __half** wpack_dev, float** bias_dev, size_t* bytes, int part) {
   if (F != 256 || n_blocks != kBodyLayers / 2 || d_in != kDin || n_coarse != 64 || n_fine != 128)
     return cudaErrorInvalidValue;
   std::vector<__half> img((size_t)kStagesPerTile * kStageBytes / 2, __float2half(0.f));
   std::vector<float> bias((size_t)kBiasLayers * 256, 0.f);
+  // part 0: fp16(w); part 1: fp16(4096 (w - fp16(w))), the low half of mlp_precise.cu's split
   auto put = [&](int stage, int r, int k, float v) {
     size_t off = (size_t)stage * kStageBytes + tc::sw128_offset(r, k >> 3) + (k & 7) * 2;
-    img[off / 2] = __float2half_rn(v);
+    const __half hi = __float2half_rn(v);
+    img[off / 2] = part == 0 ? hi : __float2half_rn((v - __half2float(hi)) * 4096.f);
   };
   size_t p = 0;
   const float* Wh = P + p; p += (size_t)F * d_in;
@@ -780,9 +782,11 @@ cudaError_t tc_pack_weights(const float* P, int d_in, int F, int n_blocks, int n
   for (int o = 0; o < n_coarse + 1; ++o) bt[128 + o] = ba[o];
   *bytes = img.size() * sizeof(__half);
   cudaError_t e = cudaMalloc(wpack_dev, *bytes);
-  if (e == cudaSuccess) e = cudaMalloc(bias_dev, bias.size() * sizeof(float));
   if (e == cudaSuccess) e = cudaMemcpy(*wpack_dev, img.data(), *bytes, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(*bias_dev, bias.data(), bias.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (bias_dev != nullptr) {
+    if (e == cudaSuccess) e = cudaMalloc(bias_dev, bias.size() * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(*bias_dev, bias.data(), bias.size() * sizeof(float), cudaMemcpyHostToDevice);
+  }
   return e;
 }
 

@@ -143,6 +143,26 @@ def config5(flush, n_frames=60):
             "compose_frame_wall_ms_per_frame": api_ms}
 
 
+def trained(flush, steps=5):
+    """The config-4 placements with the GPU-distilled models (scenes/config4_trained.json,
+    2000x800, point light): trained networks populate many fine bins, so the near-tie
+    guard carries a large share of the evaluations."""
+    from paper_2308_04669_b200 import scene as S
+    desc = S.load_scene(ROOT / "scenes" / "config4_trained.json")
+    inst = desc.instantiate()
+    cam = desc.camera()
+    rnd = pipeline.FrameRenderer(inst, cam, desc.build_lights(), desc.render_config())
+    _lib.context().set_option(_lib.OPT_PROFILE, 1)
+    ms, st = time_frames(rnd, steps, flush)
+    _lib.context().set_option(_lib.OPT_PROFILE, 0)
+    evals = st["evals"] / steps
+    t = float(np.mean(ms))
+    return {"workload": "config4 placements, GPU-distilled models (scenes/config4_trained.json)",
+            "width": cam.width, "height": cam.height, "objects": len(inst), "ms_per_frame": t,
+            "nedf_evals_per_frame": evals, "guarded_per_frame": st["guarded"] / steps,
+            "network_ms_per_frame": st["net_ms"] / steps, "guard_ms_per_frame": st["guard_ms"] / steps}
+
+
 def sweep(flush, sizes=(1 << 16, 1 << 18, 1 << 20, 1 << 22, 1 << 24)):
     m = scenes.paper_model(0, "sphere")
     out = []
@@ -206,7 +226,7 @@ def training(flush):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="config1,config2,config3,config4,config5,sweep,train")
+    ap.add_argument("--only", default="config1,config2,config3,config4,config5,trained,sweep,train")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     which = set(args.only.split(","))
@@ -238,6 +258,8 @@ def main():
         lines.append(config5(flush))
     if "sweep" in which:
         lines.extend(sweep(flush))
+    if "trained" in which:
+        lines.append(trained(flush))
     if "train" in which:
         lines.extend(training(flush))
     if args.out:
