@@ -300,36 +300,40 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
         tc::mbar_wait(&S.dfull, dl & 1);
         tc::tc_fence_after();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {                        // 8-column chunks
-          uint32_t rm[8], rx[8];
-          tc::tmem_ld8(lane_addr + 128 * hc + 8 * j, rm);
-          tc::tmem_ld8(lane_addr + 256 + 128 * hc + 8 * j, rx);
+        for (int j2 = 0; j2 < 8; ++j2) {                       // 16-column chunks: one TMEM wait each
+          uint32_t rm[16], rx[16];
+          tc::tmem_ld16(lane_addr + 128 * hc + 16 * j2, rm);
+          tc::tmem_ld16(lane_addr + 256 + 128 * hc + 16 * j2, rx);
           tc::tmem_ld_wait();
-          const float4 b_lo = *reinterpret_cast<const float4*>(bias + 8 * j);
-          const float4 b_hi = *reinterpret_cast<const float4*>(bias + 8 * j + 4);
-          const float bb[8] = {b_lo.x, b_lo.y, b_lo.z, b_lo.w, b_hi.x, b_hi.y, b_hi.z, b_hi.w};
-          float v[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float y = (__uint_as_float(rm[i]) + __uint_as_float(rx[i]) * (1.0f / kPLo)) + bb[i];
-            const int c = 8 * j + i;
-            if (L == 0 || tail) {
-              x[c] = y;                                        // head output (no activation) / tail logits
-              v[i] = y;
-            } else if (L & 1) {
-              v[i] = fmaxf(y, 0.f);                            // fc1: h
-            } else {
-              x[c] = x[c] + fmaxf(y, 0.f);                     // fc2: residual
-              v[i] = x[c];
+          for (int jh = 0; jh < 2; ++jh) {
+            const int j = 2 * j2 + jh;                         // 8-column group
+            const float4 b_lo = *reinterpret_cast<const float4*>(bias + 8 * j);
+            const float4 b_hi = *reinterpret_cast<const float4*>(bias + 8 * j + 4);
+            const float bb[8] = {b_lo.x, b_lo.y, b_lo.z, b_lo.w, b_hi.x, b_hi.y, b_hi.z, b_hi.w};
+            float v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float y = (__uint_as_float(rm[8 * jh + i]) + __uint_as_float(rx[8 * jh + i]) * (1.0f / kPLo)) + bb[i];
+              const int c = 8 * j + i;
+              if (L == 0 || tail) {
+                x[c] = y;                                      // head output (no activation) / tail logits
+                v[i] = y;
+              } else if (L & 1) {
+                v[i] = fmaxf(y, 0.f);                          // fc1: h
+              } else {
+                x[c] = x[c] + fmaxf(y, 0.f);                   // fc2: residual
+                v[i] = x[c];
+              }
             }
-          }
-          if (!tail) {
-            // next layer's input, K columns 128 hc + 8 j .. + 7: atom (2 hc + j / 8), chunk j % 8
-            uint4 h, l;
-            split8(v, h, l);
-            const uint32_t o = (2 * hc + (j >> 3)) * kPAtom + tc::sw128_offset(row, j & 7);
-            *reinterpret_cast<uint4*>(S.a + o) = h;
-            *reinterpret_cast<uint4*>(S.a + 4 * kPAtom + o) = l;
+            if (!tail) {
+              // next layer's input, K columns 128 hc + 8 j .. + 7: atom (2 hc + j / 8), chunk j % 8
+              uint4 h, l;
+              split8(v, h, l);
+              const uint32_t o = (2 * hc + (j >> 3)) * kPAtom + tc::sw128_offset(row, j & 7);
+              *reinterpret_cast<uint4*>(S.a + o) = h;
+              *reinterpret_cast<uint4*>(S.a + 4 * kPAtom + o) = l;
+            }
           }
         }
         tc::tc_fence_before();
