@@ -61,6 +61,11 @@ int nedf_diag_cl_trace(int enable, unsigned long long* out, int n);
  * [160+L] layer landed, [200+L] next B tiles written, [240+q] weight stage q issued; n <= 320. */
 int nedf_diag_guard_trace(int enable, unsigned long long* out, int n);
 
+/* Timeline of CTA 0's first tile in the guard's throughput kernel (mlp_precise.cu, clock64):
+ * [L] layer L's MMAs start, [40+L] issued, [80+L] epilogue has the accumulators, [120+L]
+ * epilogue done, [160+p] head point p encoded; n <= 200. */
+int nedf_diag_precise_trace(int enable, unsigned long long* out, int n);
+
 /* tcgen05 issue-rate probe: `iters` M=128 x N MMAs (ts: A from TMEM) from one
  * warp, committing every `per_commit`; writes elapsed clock64 cycles to out_dev. */
 int nedf_diag_mma_rate(int ts, int n, int iters, int per_commit, unsigned long long* out_dev);

@@ -72,15 +72,21 @@ __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   uint32_t h[4], l[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const __half a = __float2half_rn(v[2 * i]), b = __float2half_rn(v[2 * i + 1]);
-    h[i] = (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
-    l[i] = h2_pack((v[2 * i] - __half2float(a)) * kPLo, (v[2 * i + 1] - __half2float(b)) * kPLo);
+    const __half2 hh = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+    const float2 hf = __half22float2(hh);
+    h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[i] = h2_pack((v[2 * i] - hf.x) * kPLo, (v[2 * i + 1] - hf.y) * kPLo);
   }
   hi = make_uint4(h[0], h[1], h[2], h[3]);
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
 }  // namespace
+
+// timeline of CTA 0's first tile (diagnostics): [L] layer L's MMAs start, [40 + L] issued,
+// [80 + L] epilogue has the accumulators, [120 + L] epilogue done (warp 8), [160 + p] head point p encoded
+__device__ unsigned long long g_ptrace[200];
+__device__ int g_ptrace_on;
 
 __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt, ListSet ls, RayJob job,
                                                                    OutSpec out, int min_tiles16) {
@@ -119,6 +125,11 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
   tc::tc_fence_after();
   const uint32_t tbase = S.tmem_base;
   const int total = S.tiles[ng];
+  const bool trace = g_ptrace_on && blockIdx.x == 0 && lane == 0;
+#define PTRACE(i, cond) \
+  do {                  \
+    if (trace && (cond)) g_ptrace[(i)] = clock64(); \
+  } while (0)
   auto lookup = [&](int t, int& g, int64_t& base, int& n) {
     g = 0;
     while (g < ng - 1 && t >= S.tiles[g + 1]) ++g;
@@ -163,6 +174,7 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
             tc::mbar_wait(&S.aready, bl & 1);
             ++bl;
           }
+          PTRACE(L, t == (int)blockIdx.x);
           const int npt = L == 0 ? 16 : 1;                    // head: per point; body: one pass
           for (int pt = 0; pt < npt; ++pt) {
             uint32_t a_hi = a0, a_lo = a0 + 4 * kPAtom;
@@ -204,6 +216,7 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
           }
           if (tc::elect_one()) tc::mma_commit(&S.dfull);
           __syncwarp();
+          PTRACE(40 + L, t == (int)blockIdx.x);
         }
       }
     }
@@ -279,6 +292,7 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
         tc::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&S.afull[slot]);
+        if (warp == 4) PTRACE(160 + pt, t == (int)blockIdx.x);
       }
     }
   } else {
@@ -299,8 +313,19 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
         const float* bias = m.bias_pack + L * 256 + 128 * hc;
         tc::mbar_wait(&S.dfull, dl & 1);
         tc::tc_fence_after();
+        if (warp == 8) PTRACE(80 + L, t == (int)blockIdx.x);
+#pragma unroll
 #pragma unroll
         for (int j2 = 0; j2 < 8; ++j2) {                       // 16-column chunks: one TMEM wait each
+          float bb2[16];                                       // bias first: its latency overlaps TMEM's
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 b4 = *reinterpret_cast<const float4*>(bias + 16 * j2 + 4 * i);
+            bb2[4 * i] = b4.x;
+            bb2[4 * i + 1] = b4.y;
+            bb2[4 * i + 2] = b4.z;
+            bb2[4 * i + 3] = b4.w;
+          }
           uint32_t rm[16], rx[16];
           tc::tmem_ld16(lane_addr + 128 * hc + 16 * j2, rm);
           tc::tmem_ld16(lane_addr + 256 + 128 * hc + 16 * j2, rx);
@@ -308,9 +333,7 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
 #pragma unroll
           for (int jh = 0; jh < 2; ++jh) {
             const int j = 2 * j2 + jh;                         // 8-column group
-            const float4 b_lo = *reinterpret_cast<const float4*>(bias + 8 * j);
-            const float4 b_hi = *reinterpret_cast<const float4*>(bias + 8 * j + 4);
-            const float bb[8] = {b_lo.x, b_lo.y, b_lo.z, b_lo.w, b_hi.x, b_hi.y, b_hi.z, b_hi.w};
+            const float* bb = bb2 + 8 * jh;
             float v[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -342,6 +365,7 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&S.aready);
         }
+        if (warp == 8) PTRACE(120 + L, t == (int)blockIdx.x);
       }
       // ---- decode (model.py:277-293): slice 0 = fine logits, slice 1 = coarse (0-63) and alpha (64)
       const bool valid = row < n;
@@ -383,6 +407,13 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<512>(tbase);
+}
+
+extern "C" int nedf_diag_precise_trace(int enable, unsigned long long* out, int n) {
+  if (enable >= 0 && cudaMemcpyToSymbol(g_ptrace_on, &enable, sizeof(int)) != cudaSuccess) return NEDF_ERR_CUDA;
+  if (out && n > 0 && cudaMemcpyFromSymbol(out, g_ptrace, (n < 200 ? n : 200) * sizeof(unsigned long long)) != cudaSuccess)
+    return NEDF_ERR_CUDA;
+  return NEDF_OK;
 }
 
 cudaError_t launch_mlp_precise(const GroupTable& gt, const ListSet& ls, const RayJob& job, const OutSpec& out,
