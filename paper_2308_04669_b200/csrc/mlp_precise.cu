@@ -20,16 +20,20 @@
 // halves (~2^-23): float32-level.  The residual stream stays fp32 in the
 // epilogue's registers.
 //
-// Per CTA (16 warps): warp 0 streams [W_hi | W_lo] stages (32 KB each) through
+// Per CTA (20 warps): warp 0 streams [W_hi | W_lo] stages (32 KB each) through
 // a 3-slot ring; warp 1 issues the MMAs (both operands from shared memory:
 // the layer input's hi / lo tiles, 128 KB, are written by the epilogue); warps
-// 4-7 encode the head input per point (float64 sincospi + double-angle steps)
-// into four 32 KB slots of the same region; warps 8-15 are the epilogue
-// (thread = ray x 128-column slice): main + cross, bias, ReLU / residual, the
-// next layer's hi / lo tiles; the tail's logits are decoded here (first-max
-// argmax, alpha, world depth, z-buffer atomicMin) like the other kernels.
-// Layers run back to back (the epilogue rewrites the one input buffer), so
-// per layer: 96 MMAs + the epilogue.
+// 4-19 are 4 worker groups of 4 warps (one per TMEM lane quadrant, thread =
+// ray).  Head: group g encodes points g, g + 4, ... (float64 sincospi +
+// double-angle steps) into 32 KB slot g of the same region.  Body: group g is
+// the epilogue of output columns [64 g, 64 g + 64): main + cross, bias, ReLU /
+// residual, the next layer's hi / lo atom g; the tail's logits are decoded
+// across the groups (first-max argmax, alpha, world depth, z-buffer
+// atomicMin) like the other kernels.  Layers run back to back (the epilogue
+// rewrites the one input buffer), so per layer: 96 MMAs (~6.9k cycles) + the
+// epilogue (~4.7k with four warps per SM sub-partition; 10k with two).
+// Registers: 640 threads launch at 96; warps 0-3 release theirs so the
+// workers run at 112.
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -42,7 +46,7 @@
 namespace nedf {
 namespace {
 
-constexpr int kPThreads = 512;
+constexpr int kPThreads = 640;                  // 20 warps: producer, MMA, 2 idle, 16 workers
 constexpr uint32_t kPStage = 16384;             // one [128 N x 64 K] fp16 weight stage (hi or lo)
 constexpr int kPRing = 3;                       // slots of [hi | lo] stage pairs (32 KB)
 constexpr int kPHeadStages = 32;                // 16 points x 2 slices
@@ -56,13 +60,19 @@ struct PSmem {
   unsigned char ring[kPRing][2 * kPStage];
   uint64_t full[kPRing], empty[kPRing];
   uint64_t afull[4], aempty[4];                 // head slots: encoders -> MMA, MMA -> encoders
-  uint64_t aready;                              // body input written (8 epilogue warps)
+  uint64_t aready;                              // body input written (16 worker warps)
   uint64_t dfull;                               // a layer's accumulators complete
-  uint64_t tfree;                               // the tile's tail done: the input region may take the next head
   uint32_t tmem_base;
   int tiles[65];
-  int dec_c[128];
-  float dec_a[128];
+};
+
+// tail decode scratch (the first 2 KB of head slot 0: free once the tail's MMAs are done,
+// rewritten only by worker group 0's next head, after its decode)
+struct PDecode {
+  float fine_best[128];                         // group 1: max of fine logits 64-127
+  int fine_idx[128];                            //          and its first index
+  int coarse[128];                              // group 2: coarse argmax
+  float alpha[128];                             // group 3: the alpha logit
 };
 
 __device__ __forceinline__ uint32_t h2_pack(float a, float b) { return tc::pack_h2(a, b); }
@@ -114,9 +124,8 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
     }
     for (int i = 0; i < kPRing; ++i) { tc::mbar_init(&S.full[i], 1); tc::mbar_init(&S.empty[i], 1); }
     for (int i = 0; i < 4; ++i) { tc::mbar_init(&S.afull[i], 4); tc::mbar_init(&S.aempty[i], 1); }
-    tc::mbar_init(&S.aready, 8);
+    tc::mbar_init(&S.aready, 16);
     tc::mbar_init(&S.dfull, 1);
-    tc::mbar_init(&S.tfree, 8);
     tc::mbar_fence_init();
   }
   if (warp == 1) tc::tmem_alloc<512>(&S.tmem_base);     // main[2] cols 0-255, cross[2] cols 256-511
@@ -139,7 +148,8 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
   };
 
   if (warp < 4) {
-    tc::reg_dealloc<40>();
+    // registers: 640 threads launch at 96; the 16 workers take 112 from what warps 0-3 release
+    if (warp < 2) tc::reg_dealloc<32>(); else tc::reg_dealloc<24>();
     if (warp == 0) {
       // ------------------------------------------------------------------ weight producer
       uint32_t gq = 0;
@@ -220,120 +230,110 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
         }
       }
     }
-  } else if (warp < 8) {
-    tc::reg_dealloc<120>();
-    // -------------------------------------------------------------------- encoders (thread = ray)
-    const int row = tid - 128;
-    uint32_t hq = 0, tfc = 0;
+  } else {
+    tc::reg_alloc<112>();
+    // ---------------------------------------------------------------------- workers
+    // 16 warps in 4 groups; group sl = warps 4 + 4 sl .. 7 + 4 sl covers the four TMEM lane
+    // quadrants (warp & 3), thread = ray (row).  Head: group sl encodes points sl, sl + 4, ...
+    // into head slot sl.  Body: group sl owns output columns [64 sl, 64 sl + 64) -- the
+    // epilogue (main + cross, bias, ReLU / residual, the next layer's hi / lo atom sl).
+    const int q = warp & 3, sl = (warp - 4) >> 2;
+    const int row = 32 * q + lane;
+    const uint32_t lane_addr = tbase + ((uint32_t)(32 * q) << 16) + 64 * sl;
+    uint32_t dl = 0, use = 0;
+    float x[64];                                             // residual stream: columns [64 sl, 64 sl + 64)
+    PDecode& D = *reinterpret_cast<PDecode*>(S.a);
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int g, n;
       int64_t b0;
       lookup(t, g, b0, n);
       const DevModel& m = gt.models[g];
       const bool valid = row < n;
-      double lo3[3] = {0, 0, 0}, ld3[3] = {0, 0, 0}, t0 = 0, t1 = 0;
-      uint32_t pix = 0;
-      if (valid) {
-        pix = ls.pix[b0 + row];
-        if (!feats_in) {
-          double wo[3], wd[3];
-          item_local_ray(job, pix, ls.obj[b0 + row], wo, wd, lo3, ld3);
-          slab_clip(lo3, ld3, m.bmin, m.bmax, t0, t1);
-        }
-      }
-      if (t != (int)blockIdx.x) {                            // the previous tile's tail has left the region
-        tc::mbar_wait(&S.tfree, tfc & 1);
-        ++tfc;
-      }
-      for (int pt = 0; pt < 16; ++pt, ++hq) {
-        const int slot = hq & 3;
-        if (pt >= 4) tc::mbar_wait(&S.aempty[slot], ((hq >> 2) - 1) & 1);
-        float f[64];
-        if (!valid) {
-#pragma unroll
-          for (int j = 0; j < 64; ++j) f[j] = 0.f;
-        } else if (feats_in) {
-          const float* src = out.feats + (size_t)pix * kDin + pt * kPerPoint;
-#pragma unroll
-          for (int j = 0; j < 63; ++j) f[j] = src[j];
-          f[63] = 0.f;
-        } else {
-          // geometry.py:312-342 in float64: sincospi at level 0, double-angle steps for 1-9
-          const double tt = t0 + (t1 - t0) * lin16(pt);
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            const double p = ((lo3[a] + tt * ld3[a]) - m.c[a]) / m.h[a];
-            f[21 * a] = (float)p;
-            double sn, cs;
-            sincospi(p, &sn, &cs);
-            f[21 * a + 1] = (float)sn;
-            f[21 * a + 2] = (float)cs;
-#pragma unroll
-            for (int k = 1; k < kLevels; ++k) {
-              const double s2 = 2.0 * sn * cs, c2 = (cs - sn) * (cs + sn);
-              sn = s2;
-              cs = c2;
-              f[21 * a + 1 + 2 * k] = (float)sn;
-              f[21 * a + 2 + 2 * k] = (float)cs;
-            }
+      // ---- head input: 16 points x 64 features (geometry.py:312-342 in float64)
+      {
+        double lo3[3] = {0, 0, 0}, ld3[3] = {0, 0, 0}, t0 = 0, t1 = 0;
+        uint32_t pix = 0;
+        if (valid) {
+          pix = ls.pix[b0 + row];
+          if (!feats_in) {
+            double wo[3], wd[3];
+            item_local_ray(job, pix, ls.obj[b0 + row], wo, wd, lo3, ld3);
+            slab_clip(lo3, ld3, m.bmin, m.bmax, t0, t1);
           }
-          f[63] = 0.f;
         }
-        unsigned char* hi = S.a + slot * 2 * kPAtom;
+        unsigned char* hi = S.a + sl * 2 * kPAtom;
         unsigned char* lo = hi + kPAtom;
+        for (int pt = sl; pt < 16; pt += 4, ++use) {
+          // earlier uses of this slot (this tile's) must have left the tensor pipe; the previous
+          // tile's are done (its tail's accumulators were read after all of its MMAs)
+          if (pt >= 4) tc::mbar_wait(&S.aempty[sl], (use - 1) & 1);
+          float f[64];
+          if (!valid) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint4 h, l;
-          split8(f + 8 * c, h, l);
-          const uint32_t o = tc::sw128_offset(row, c);
-          *reinterpret_cast<uint4*>(hi + o) = h;
-          *reinterpret_cast<uint4*>(lo + o) = l;
+            for (int j = 0; j < 64; ++j) f[j] = 0.f;
+          } else if (feats_in) {
+            const float* src = out.feats + (size_t)pix * kDin + pt * kPerPoint;
+#pragma unroll
+            for (int j = 0; j < 63; ++j) f[j] = src[j];
+            f[63] = 0.f;
+          } else {
+            const double tt = t0 + (t1 - t0) * lin16(pt);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              const double p = ((lo3[a] + tt * ld3[a]) - m.c[a]) / m.h[a];
+              f[21 * a] = (float)p;
+              double sn, cs;
+              sincospi(p, &sn, &cs);
+              f[21 * a + 1] = (float)sn;
+              f[21 * a + 2] = (float)cs;
+#pragma unroll
+              for (int k = 1; k < kLevels; ++k) {
+                const double s2 = 2.0 * sn * cs, c2 = (cs - sn) * (cs + sn);
+                sn = s2;
+                cs = c2;
+                f[21 * a + 1 + 2 * k] = (float)sn;
+                f[21 * a + 2 + 2 * k] = (float)cs;
+              }
+            }
+            f[63] = 0.f;
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint4 h, l;
+            split8(f + 8 * c, h, l);
+            const uint32_t o = tc::sw128_offset(row, c);
+            *reinterpret_cast<uint4*>(hi + o) = h;
+            *reinterpret_cast<uint4*>(lo + o) = l;
+          }
+          tc::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&S.afull[sl]);
+          if (warp == 4) PTRACE(160 + pt, t == (int)blockIdx.x);
         }
-        tc::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&S.afull[slot]);
-        if (warp == 4) PTRACE(160 + pt, t == (int)blockIdx.x);
       }
-    }
-  } else {
-    tc::reg_alloc<176>();
-    // -------------------------------------------------------------------- epilogue (thread = ray x slice)
-    const int q = warp & 3, hc = (warp - 8) >> 2;            // TMEM lane quadrant, output slice
-    const int row = 32 * q + lane;
-    const uint32_t lane_addr = tbase + ((uint32_t)(32 * q) << 16);
-    uint32_t dl = 0;
-    float x[128];                                            // residual stream: columns [128 hc, 128 hc + 128)
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      int g, n;
-      int64_t b0;
-      lookup(t, g, b0, n);
-      const DevModel& m = gt.models[g];
+      // ---- layers
       for (int L = 0; L < kPBodyLayers + 2; ++L, ++dl) {
         const bool tail = L == kPBodyLayers + 1;
-        const float* bias = m.bias_pack + L * 256 + 128 * hc;
+        const float* bias = m.bias_pack + L * 256 + 64 * sl;
         tc::mbar_wait(&S.dfull, dl & 1);
         tc::tc_fence_after();
-        if (warp == 8) PTRACE(80 + L, t == (int)blockIdx.x);
+        if (warp == 4) PTRACE(80 + L, t == (int)blockIdx.x);
 #pragma unroll
-#pragma unroll
-        for (int j2 = 0; j2 < 8; ++j2) {                       // 16-column chunks: one TMEM wait each
-          float bb2[16];                                       // bias first: its latency overlaps TMEM's
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float4 b4 = *reinterpret_cast<const float4*>(bias + 16 * j2 + 4 * i);
-            bb2[4 * i] = b4.x;
-            bb2[4 * i + 1] = b4.y;
-            bb2[4 * i + 2] = b4.z;
-            bb2[4 * i + 3] = b4.w;
-          }
+        for (int j2 = 0; j2 < 4; ++j2) {                       // 16-column chunks: one TMEM wait each
+          float4 b0 = *reinterpret_cast<const float4*>(bias + 16 * j2);   // latency overlaps TMEM's
+          float4 b1 = *reinterpret_cast<const float4*>(bias + 16 * j2 + 4);
           uint32_t rm[16], rx[16];
-          tc::tmem_ld16(lane_addr + 128 * hc + 16 * j2, rm);
-          tc::tmem_ld16(lane_addr + 256 + 128 * hc + 16 * j2, rx);
+          tc::tmem_ld16(lane_addr + 16 * j2, rm);
+          tc::tmem_ld16(lane_addr + 256 + 16 * j2, rx);
           tc::tmem_ld_wait();
 #pragma unroll
           for (int jh = 0; jh < 2; ++jh) {
             const int j = 2 * j2 + jh;                         // 8-column group
-            const float* bb = bb2 + 8 * jh;
+            if (jh == 1) {
+              b0 = *reinterpret_cast<const float4*>(bias + 16 * j2 + 8);
+              b1 = *reinterpret_cast<const float4*>(bias + 16 * j2 + 12);
+            }
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
             float v[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -350,10 +350,10 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
               }
             }
             if (!tail) {
-              // next layer's input, K columns 128 hc + 8 j .. + 7: atom (2 hc + j / 8), chunk j % 8
+              // next layer's input, K columns 64 sl + 8 j .. + 7: atom sl, chunk j
               uint4 h, l;
               split8(v, h, l);
-              const uint32_t o = (2 * hc + (j >> 3)) * kPAtom + tc::sw128_offset(row, j & 7);
+              const uint32_t o = sl * kPAtom + tc::sw128_offset(row, j);
               *reinterpret_cast<uint4*>(S.a + o) = h;
               *reinterpret_cast<uint4*>(S.a + 4 * kPAtom + o) = l;
             }
@@ -365,43 +365,39 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&S.aready);
         }
-        if (warp == 8) PTRACE(120 + L, t == (int)blockIdx.x);
+        if (warp == 4) PTRACE(120 + L, t == (int)blockIdx.x);
       }
-      // ---- decode (model.py:277-293): slice 0 = fine logits, slice 1 = coarse (0-63) and alpha (64)
-      const bool valid = row < n;
-      if (hc == 1) {
-        int cb = 0;
-        float best = x[0];
+      // ---- decode (model.py:277-293): logits 0-127 fine (groups 0, 1), 128-191 coarse
+      // (group 2), 192 alpha (group 3); first-max argmax like the other kernels
+      int best_i = 0;
+      float best = x[0];
+      if (sl < 3) {
 #pragma unroll
         for (int c = 1; c < 64; ++c)
-          if (x[c] > best) { best = x[c]; cb = c; }
-        S.dec_c[row] = cb;
-        S.dec_a[row] = x[64];
-        if (valid && out.mode == OUT_LOGITS) {
-          const size_t r = ls.pix[b0 + row];
-          for (int c = 0; c < 64; ++c) out.lc[r * 64 + c] = x[c];
-          out.la[r] = x[64];
-        }
+          if (x[c] > best) { best = x[c]; best_i = c; }
       }
-      tc::named_bar(1, 256);
-      if (hc == 0 && valid) {
-        const uint32_t pix = ls.pix[b0 + row], obj = ls.obj[b0 + row];
-        if (out.mode == OUT_LOGITS) {
-          for (int c = 0; c < 128; ++c) out.lf[(size_t)pix * 128 + c] = x[c];
+      const size_t pix_l = valid ? (size_t)ls.pix[b0 + row] : 0;
+      if (valid && out.mode == OUT_LOGITS) {
+        if (sl < 2) {
+          for (int c = 0; c < 64; ++c) out.lf[pix_l * 128 + 64 * sl + c] = x[c];
+        } else if (sl == 2) {
+          for (int c = 0; c < 64; ++c) out.lc[pix_l * 64 + c] = x[c];
         } else {
-          int fb = 0;
-          float best = x[0];
-#pragma unroll
-          for (int c = 1; c < 128; ++c)
-            if (x[c] > best) { best = x[c]; fb = c; }
-          double wo[3], wd[3], lo[3], ld[3];
-          item_local_ray(job, pix, obj, wo, wd, lo, ld);
-          finish_ray(m, job, out, pix, obj, S.dec_c[row], fb, (double)S.dec_a[row], wo, wd);
+          out.la[pix_l] = x[0];
         }
       }
-      tc::named_bar(1, 256);                                  // dec_* reused by the next tile
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&S.tfree);
+      if (sl == 1) { D.fine_best[row] = best; D.fine_idx[row] = 64 + best_i; }
+      if (sl == 2) D.coarse[row] = best_i;
+      if (sl == 3) D.alpha[row] = x[0];
+      tc::named_bar(1, 512);
+      if (sl == 0 && valid && out.mode != OUT_LOGITS) {
+        const int fb = D.fine_best[row] > best ? D.fine_idx[row] : best_i;
+        const uint32_t obj = ls.obj[b0 + row];
+        double wo[3], wd[3], lo[3], ld[3];
+        item_local_ray(job, (uint32_t)pix_l, obj, wo, wd, lo, ld);
+        finish_ray(m, job, out, (uint32_t)pix_l, obj, D.coarse[row], fb, (double)D.alpha[row], wo, wd);
+      }
+      if (sl == 0) tc::named_bar(2, 128);                    // all of group 0 has read D before slot 0 is rewritten
     }
   }
   tc::tc_fence_before();
