@@ -70,7 +70,11 @@ enum {
   NEDF_OPT_FUSE = 8,            /* 1 (default) = nedf_render_frame fuses the per-pixel passes (STEP 1 resolve,
                                    STEP 2, shadow fill, first light's STEP 3 setup; last light's resolve +
                                    composite); 0 = one kernel per step, as the step entry points run */
-  NEDF_OPT_GUARD_KERNEL = 9     /* one of NEDF_GUARD_*: which kernel re-evaluates the near-tie rays */
+  NEDF_OPT_GUARD_KERNEL = 9,    /* one of NEDF_GUARD_*: which kernel re-evaluates the near-tie rays */
+  NEDF_OPT_CULL = 10            /* 1 (default) = STEP 1 front-first culling: a pixel's pair with the nearest
+                                   depth bound is evaluated first, the others only if their bound
+                                   |(o - T).d| - s mu_max can still beat its result (same z-buffer, fewer
+                                   evaluations); off with a plane cache.  0 = every box hit evaluated */
 };
 /* Near-tie guard kernels (NEDF_OPT_GUARD_KERNEL); all fp32-accurate. */
 enum {
@@ -191,6 +195,7 @@ typedef struct {
   double guard_ms;          /* summed device time of the fp32 re-evaluation of guarded rays */
   int64_t h2d_bytes;        /* host->device bytes this library copied (per-call scene tables) */
   int64_t exact_clips;      /* (ray, object) box tests the certified fp32 test left to float64 */
+  int64_t culled;           /* STEP 1 box hits skipped by front-first culling (NEDF_OPT_CULL) */
 } NedfStepStats;
 
 /* ---- library / context ---------------------------------------------------- */

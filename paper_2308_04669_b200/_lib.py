@@ -25,7 +25,7 @@ NEDF_ERR_NOMEM = -5
 
 PREC_AUTO, PREC_TENSOR, PREC_FP32 = 0, 1, 2
 OPT_PRECISION, OPT_GUARD_PPM, OPT_TC_CTAS, OPT_PROFILE, OPT_TC_KERNEL, OPT_GUARD_CLUSTER = 1, 2, 3, 4, 5, 6
-OPT_SETUP_EXACT, OPT_FUSE, OPT_GUARD_KERNEL = 7, 8, 9
+OPT_SETUP_EXACT, OPT_FUSE, OPT_GUARD_KERNEL, OPT_CULL = 7, 8, 9, 10
 GUARD_AUTO, GUARD_TCGEN05, GUARD_MMA_SYNC, GUARD_PRECISE = 0, 1, 2, 3
 TC_AUTO, TC_SINGLE, TC_MCAST2, TC_MCAST4 = 0, 1, 3, 4
 
@@ -74,7 +74,8 @@ class NedfFrameBuffers(C.Structure):
 class NedfStepStats(C.Structure):
     _fields_ = [("evals", C.c_int64), ("guarded", C.c_int64), ("covered", C.c_int64), ("resampled", C.c_int64),
                 ("launches", C.c_int64), ("net_launches", C.c_int64), ("net_ms", C.c_double),
-                ("guard_ms", C.c_double), ("h2d_bytes", C.c_int64), ("exact_clips", C.c_int64)]
+                ("guard_ms", C.c_double), ("h2d_bytes", C.c_int64), ("exact_clips", C.c_int64),
+                ("culled", C.c_int64)]
 
 
 P = C.c_void_p
@@ -196,7 +197,8 @@ class Context:
         check(self._lib.nedf_read_stats(self.handle, C.byref(s), stream))
         return {"evals": s.evals, "guarded": s.guarded, "covered": s.covered, "resampled": s.resampled,
                 "launches": s.launches, "net_launches": s.net_launches, "net_ms": s.net_ms,
-                "guard_ms": s.guard_ms, "h2d_bytes": s.h2d_bytes, "exact_clips": s.exact_clips}
+                "guard_ms": s.guard_ms, "h2d_bytes": s.h2d_bytes, "exact_clips": s.exact_clips,
+                "culled": s.culled}
 
     _RESET_SLOT = 63                     # mapped slot 63 only absorbs resets; 0-62 rotate
 
@@ -228,7 +230,7 @@ class Context:
         s = NedfStepStats()
         check(self._lib.nedf_stats_slot(self.handle, slot, C.byref(s)))
         return {"evals": s.evals, "guarded": s.guarded, "covered": s.covered, "resampled": s.resampled,
-                "exact_clips": s.exact_clips}
+                "exact_clips": s.exact_clips, "culled": s.culled}
 
     def __del__(self):
         try:

@@ -79,6 +79,7 @@ struct NedfContext {
   int guard_kernel = NEDF_GUARD_AUTO;
   int setup_exact = 0;
   int fuse = 1;
+  int cull = 1;
   int guard_direct = 0;      // diagnostics: run only the guard kernel NEDF_GUARD_* on every list entry
   int profile = 0;
   int64_t launches = 0;
@@ -87,7 +88,7 @@ struct NedfContext {
   std::vector<std::pair<int, int>> ev_pairs;   // (start index, kind)
   size_t ev_used = 0;
   DevBuf models, objs, fields, rows, offsets, counts, redo_counts, lists_pix, lists_obj, redo_pix, redo_obj,
-      key, skey, stats, tile_counter;
+      key, skey, stats, tile_counter, defer_pix, defer_obj, defer_low, defer_count;
   int64_t h2d_bytes = 0;
   // mapped pinned mirror of the 8 stats counters: read back by a one-warp kernel, so reading stats
   // never queues behind a caller's large device-to-host copy on the copy engine
@@ -190,6 +191,10 @@ int build_scene(NedfContext* ctx, const NedfObject* objs, int n_objs, const Nedf
           d.bmaxf[i] = (float)hm.bmax[i];
         }
         d.inv_sf = (float)(1.0 / o.s);
+        // s * mu_max, mu_max = decode_mu(N_c - 1, N_f - 1) (model.py:89-92), rounded up
+        const double mu_max = 2.0 * hm.l * ((double)(hm.n_coarse - 1) / hm.n_coarse) +
+                              (2.0 * hm.l / hm.n_coarse) * ((double)(hm.n_fine - 1) / hm.n_fine) - hm.l;
+        d.smu_f = std::nextafter((float)(o.s * mu_max), INFINITY);
       }
       if (!o.model->host.tensor_ok) sc.all_tc = false;
     } else if (o.depth_kind == NEDF_DEPTH_ANALYTIC) {
@@ -342,6 +347,7 @@ int prepare_frame(NedfContext* ctx, const NedfCamera* cam, const NedfObject* obj
   CUDA_TRY(ctx->skey.ensure(std::max<int64_t>(F.n_pix, 1) * sizeof(unsigned long long)));
   CUDA_TRY(ctx->stats.ensure(8 * sizeof(unsigned long long)));
   CUDA_TRY(ctx->tile_counter.ensure(64 * sizeof(int)));
+  CUDA_TRY(ctx->defer_count.ensure(sizeof(int)));
 
   F.gt.models = ctx->models.as<DevModel>();
   F.gt.n_groups = ng;
@@ -406,8 +412,11 @@ int prof_mark(NedfContext* ctx, cudaStream_t st, int kind, bool start) {
   } while (0)
 
 // Evaluate the network on every list entry with the context's precision.
+// two_pass: F.fj.defer holds STEP 1's deferred pairs (front-first culling) -- the
+// network runs on the front pairs, then on the deferred ones that can still win.
 int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& out, cudaStream_t st) {
   if (F.gt.n_groups == 0) return NEDF_OK;
+  const bool two_pass = job.mode == RAY_PRIMARY && F.fj.defer.pix != nullptr && out.mode == OUT_ZBUF;
   if (ctx->guard_direct) {
     if (ctx->guard_direct == NEDF_GUARD_TCGEN05) LAUNCH(ctx, launch_guard_tc(F.gt, F.ls, job, out, ctx->n_sms, st));
     else if (ctx->guard_direct == NEDF_GUARD_PRECISE) LAUNCH(ctx, launch_mlp_precise(F.gt, F.ls, job, out, ctx->n_sms, -1, st));
@@ -426,12 +435,20 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
     CUDA_TRY(cudaMemsetAsync(a.tile_counter, 0, 64 * sizeof(int), st));
     int ctas = ctx->tc_ctas > 0 ? ctx->tc_ctas : ctx->n_sms;
     if ((rc = prof_mark(ctx, st, 0, true))) return rc;
-    switch (ctx->tc_kernel) {
-      case NEDF_TC_SINGLE: LAUNCH(ctx, launch_mlp_tc(a, ctas, 1, st)); break;
-      case NEDF_TC_MCAST4: LAUNCH(ctx, launch_mlp_tc(a, ctas, 4, st)); break;
-      default: LAUNCH(ctx, launch_mlp_tc(a, ctas, 2, st)); break;
-    }
+    const int mc = ctx->tc_kernel == NEDF_TC_SINGLE ? 1 : ctx->tc_kernel == NEDF_TC_MCAST4 ? 4 : 2;
+    LAUNCH(ctx, launch_mlp_tc(a, ctas, mc, st));
     if ((rc = prof_mark(ctx, st, 0, false))) return rc;
+    if (two_pass) {
+      // front-first culling: the deferred pairs that can still win, then one guard for both passes
+      add_counts_kernel<<<1, 32, 0, st>>>(F.ls.count, F.redo.count, F.gt.n_groups, F.fj.stats, 0);
+      ctx->launches += 1;
+      CUDA_TRY(cudaMemsetAsync(F.ls.count, 0, 64 * sizeof(int), st));
+      LAUNCH(ctx, launch_defer_filter(F.fj, F.ls, ctx->n_sms, st));
+      CUDA_TRY(cudaMemsetAsync(a.tile_counter, 0, 64 * sizeof(int), st));
+      if ((rc = prof_mark(ctx, st, 0, true))) return rc;
+      LAUNCH(ctx, launch_mlp_tc(a, ctas, mc, st));
+      if ((rc = prof_mark(ctx, st, 0, false))) return rc;
+    }
     if (a.use_guard) {
       if ((rc = prof_mark(ctx, st, 1, true))) return rc;
       // 8-CTA clusters halve the MMA work per layer on a CTA's critical path but only ~18 fit at
@@ -457,11 +474,20 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
     ctx->launches += 1;
   } else {
     if ((rc = prof_mark(ctx, st, 0, true))) return rc;
-    if (F.sc.all_tc && tc_available() && out.feats == nullptr)
-      LAUNCH(ctx, launch_mlp_fp32_stream(F.gt, F.ls, job, out, ctx->n_sms, 32, st));
-    else
-      LAUNCH(ctx, launch_mlp_fp32(F.gt, F.ls, job, out, ctx->n_sms, st));
-    if ((rc = prof_mark(ctx, st, 0, false))) return rc;
+    for (int pass = 0; pass < (two_pass ? 2 : 1); ++pass) {
+      if (pass == 1) {
+        add_counts_kernel<<<1, 32, 0, st>>>(F.ls.count, F.redo.count, F.gt.n_groups, F.fj.stats, 0);
+        ctx->launches += 1;
+        CUDA_TRY(cudaMemsetAsync(F.ls.count, 0, 64 * sizeof(int), st));
+        LAUNCH(ctx, launch_defer_filter(F.fj, F.ls, ctx->n_sms, st));
+        if ((rc = prof_mark(ctx, st, 0, true))) return rc;
+      }
+      if (F.sc.all_tc && tc_available() && out.feats == nullptr)
+        LAUNCH(ctx, launch_mlp_fp32_stream(F.gt, F.ls, job, out, ctx->n_sms, 32, st));
+      else
+        LAUNCH(ctx, launch_mlp_fp32(F.gt, F.ls, job, out, ctx->n_sms, st));
+      if ((rc = prof_mark(ctx, st, 0, false))) return rc;
+    }
     add_counts_kernel<<<1, 32, 0, st>>>(F.ls.count, F.redo.count, F.gt.n_groups, F.fj.stats, 0);
     ctx->launches += 1;
   }
@@ -475,6 +501,22 @@ int do_step1(NedfContext* ctx, Frame& F, cudaStream_t st, bool resolve = true) {
   fj.ray.mode = RAY_PRIMARY;
   CUDA_TRY(cudaMemsetAsync(F.ls.count, 0, 64 * sizeof(int), st));
   if (F.n_pix == 0) return NEDF_OK;
+  // front-first culling: worth it with two or more NeDF objects; not with a plane cache (every
+  // plane is an output) or a direct guard run (diagnostics evaluate the lists as built)
+  int n_nedf = 0;
+  for (const DevObj& o : F.sc.objs) n_nedf += o.depth_kind == NEDF_DEPTH_NEDF ? 1 : 0;
+  memset(&fj.defer, 0, sizeof(fj.defer));
+  if (ctx->cull && n_nedf >= 2 && fj.planes == nullptr && !ctx->guard_direct && F.sc.n_objs <= 64) {
+    const int64_t cap = F.n_pix * (n_nedf - 1);
+    CUDA_TRY(ctx->defer_pix.ensure(cap * sizeof(uint32_t)));
+    CUDA_TRY(ctx->defer_obj.ensure(cap * sizeof(uint32_t)));
+    CUDA_TRY(ctx->defer_low.ensure(cap * sizeof(float)));
+    fj.defer.pix = ctx->defer_pix.as<uint32_t>();
+    fj.defer.obj = ctx->defer_obj.as<uint32_t>();
+    fj.defer.low = ctx->defer_low.as<float>();
+    fj.defer.count = ctx->defer_count.as<int>();
+    CUDA_TRY(cudaMemsetAsync(fj.defer.count, 0, sizeof(int), st));
+  }
   LAUNCH(ctx, launch_setup(fj, F.gt, F.ls, RAY_PRIMARY, ctx->setup_exact, ctx->n_sms, st));
   OutSpec out;
   memset(&out, 0, sizeof(out));
@@ -542,6 +584,7 @@ int make_shadow_job(NedfContext* ctx, const Frame& F, const NedfObject* objs, co
   sj.ray.depth64 = F.fj.depth;
   for (int a = 0; a < 3; ++a) sj.ray.light[a] = L->vec[a];
   sj.planes = nullptr;
+  memset(&sj.defer, 0, sizeof(sj.defer));
   sj.key = ctx->skey.as<unsigned long long>();
   return NEDF_OK;
 }
@@ -707,6 +750,9 @@ int nedf_set_option(NedfContext* c, int key, int64_t v) {
     case NEDF_OPT_FUSE:
       c->fuse = v != 0;
       return NEDF_OK;
+    case NEDF_OPT_CULL:
+      c->cull = v != 0;
+      return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }
@@ -723,6 +769,7 @@ int nedf_get_option(NedfContext* c, int key, int64_t* v) {
     case NEDF_OPT_SETUP_EXACT: *v = c->setup_exact; return NEDF_OK;
     case NEDF_OPT_GUARD_KERNEL: *v = c->guard_kernel; return NEDF_OK;
     case NEDF_OPT_FUSE: *v = c->fuse; return NEDF_OK;
+    case NEDF_OPT_CULL: *v = c->cull; return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }
@@ -754,6 +801,7 @@ int nedf_stats_slot(NedfContext* c, int slot, NedfStepStats* out) {
   out->evals = (int64_t)h[2];
   out->guarded = (int64_t)h[3];
   out->exact_clips = (int64_t)h[4];
+  out->culled = (int64_t)h[5];
   return NEDF_OK;
 }
 
@@ -773,6 +821,7 @@ int nedf_read_stats(NedfContext* c, NedfStepStats* out, void* stream) {
   out->evals = (int64_t)h[2];
   out->guarded = (int64_t)h[3];
   out->exact_clips = (int64_t)h[4];
+  out->culled = (int64_t)h[5];
   out->launches = c->launches;
   c->launches = 0;
   out->h2d_bytes = c->h2d_bytes;

@@ -65,6 +65,8 @@ struct DevObj {
   // NeDF objects, fp32 copies for the setup kernels' certified fp32 slab clip (clip_hit_f32)
   float Rf[9], Tf[3], inv_sf;       // R, T, 1/s
   float bminf[3], bmaxf[3];         // the model's relaxed box
+  float smu_f;                      // s * mu_max (rounded up): depth >= |(o - T).d| - smu_f (front-first culling)
+  int pad3;
 };
 
 // Conservative fp32 rejection before the float64 slab clip: true only when the

@@ -56,6 +56,7 @@ struct SetupObj {
   float4 sph;                    // world bounding sphere (c, 1.001 r) of the relaxed box
   float R[9], T[3], inv_s;
   float bmin[3], bmax[3];
+  float smu;                     // s * mu_max (rounded up)
   int flags;                     // bit 0: NeDF, bit 1: plane kept from the cache (skip)
 };
 
@@ -67,6 +68,7 @@ __device__ __forceinline__ SetupObj make_setup_obj(const DevObj& ob, bool cached
 #pragma unroll
   for (int i = 0; i < 3; ++i) { so.T[i] = ob.Tf[i]; so.bmin[i] = ob.bminf[i]; so.bmax[i] = ob.bmaxf[i]; }
   so.inv_s = ob.inv_sf;
+  so.smu = ob.smu_f;
   so.flags = (ob.depth_kind == NEDF_DEPTH_NEDF ? 1 : 0) | (cached && !ob.recompute ? 2 : 0);
   return so;
 }
@@ -272,6 +274,33 @@ __device__ __noinline__ int exact_box_hit(const DevObj& ob, const GroupTable& gt
   return slab_clip(lo, ld, m.bmin, m.bmax, t0, t1) ? 1 : 0;
 }
 
+// Lower bound of a NeDF pair's world depth |(o - T).d| - s mu (model.py:301-319,
+// finish_ray) over every bin pair the network can pick (mu <= mu_max), from the
+// fp32 ray: the margin covers the ray's error bounds (eo per origin component,
+// ed per direction component), T's fp32 rounding and the fp32 arithmetic.
+__device__ __forceinline__ float depth_lower_f(const SetupObj& so, const RayF& r) {
+  const float q0 = r.o[0] - so.T[0], q1 = r.o[1] - so.T[1], q2 = r.o[2] - so.T[2];
+  const float ad = fabsf(q0 * r.d[0] + q1 * r.d[1] + q2 * r.d[2]);
+  const float qn = sqrtf(q0 * q0 + q1 * q1 + q2 * q2);
+  const float margin = 2.f * (qn * (r.ed + 1e-6f) + r.eo) + 2e-6f * (ad + so.smu + amax3(so.T[0], so.T[1], so.T[2])) + 1e-6f;
+  return ad - so.smu - margin;
+}
+
+__device__ __forceinline__ void defer_append(const DeferList& df, bool take, uint32_t pix, uint32_t sidx, float low) {
+  const unsigned mask = __ballot_sync(0xffffffffu, take);
+  if (mask == 0u) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(df.count, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (take) {
+    const int at = base + __popc(mask & ((1u << lane) - 1u));
+    df.pix[at] = pix;
+    df.obj[at] = sidx;
+    df.low[at] = low;
+  }
+}
+
 template <class Ray64>
 __device__ __forceinline__ unsigned long long setup_pixel(const FrameJob& fj, const GroupTable& gt, const ListSet& ls,
                                                           const SetupObj* s_obj, unsigned long long cand, bool all_objs,
@@ -281,6 +310,12 @@ __device__ __forceinline__ unsigned long long setup_pixel(const FrameJob& fj, co
   double o[3], d[3];
   bool have64 = false;
   int k = 0;
+  // front-first culling (STEP 1): only the pair with the smallest depth bound goes to the
+  // lists now; the rest wait in fj.defer for the front pair's result (defer_filter_kernel)
+  const bool defer_on = fj.defer.pix != nullptr && mode == RAY_PRIMARY && !cached && !all_objs;
+  unsigned long long hitmask = 0ull;
+  int front = -1;
+  float front_low = INFINITY;
   while (all_objs ? k < fj.n_objs : cand != 0ull) {
     int s;
     if (all_objs) {
@@ -306,7 +341,15 @@ __device__ __forceinline__ unsigned long long setup_pixel(const FrameJob& fj, co
         }
         hit = h > 0;
       }
-      if (__any_sync(0xffffffffu, hit)) warp_append(ls, fj.ray.objs[s].group, hit, p, (uint32_t)s);
+      if (defer_on) {
+        if (hit) {
+          hitmask |= 1ull << s;
+          const float lw = depth_lower_f(so, rf);
+          if (lw < front_low) { front_low = lw; front = s; }
+        }
+      } else if (__any_sync(0xffffffffu, hit)) {
+        warp_append(ls, fj.ray.objs[s].group, hit, p, (uint32_t)s);
+      }
       if (cached && live) fj.planes[(size_t)s * fj.n_pix + p] = INFINITY;
     } else if (live) {
       if (!have64) { ray64(o, d); have64 = true; }
@@ -320,6 +363,19 @@ __device__ __forceinline__ unsigned long long setup_pixel(const FrameJob& fj, co
         key = kk < key ? kk : key;
       }
       if (cached) fj.planes[(size_t)s * fj.n_pix + p] = ok ? dep : INFINITY;
+    }
+  }
+  if (defer_on) {
+    unsigned long long any = (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)hitmask) |
+                             ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(hitmask >> 32)) << 32);
+    while (any != 0ull) {
+      const int s = __ffsll((long long)any) - 1;
+      any &= any - 1ull;
+      const bool h = (hitmask >> s) & 1ull;
+      warp_append(ls, fj.ray.objs[s].group, h && s == front, p, (uint32_t)s);
+      const bool later = h && s != front;
+      if (__any_sync(0xffffffffu, later))
+        defer_append(fj.defer, later, p, (uint32_t)s, later ? depth_lower_f(s_obj[s], rf) : 0.f);
     }
   }
   return key;
@@ -418,6 +474,41 @@ __device__ __forceinline__ double key_depth(const FrameJob& fj, const GroupTable
   double dep;
   analytic_depth(fj, ob, o, d, dep);
   return dep;
+}
+
+// Front-first culling, second half: a deferred pair is evaluated only if its depth
+// lower bound does not exceed the pixel's z-key depth after the front pairs (and
+// any analytic objects).  A skipped pair has fp32(depth) >= low > the key's fp32
+// depth, so its key could not have won the atomicMin: the z-buffer is unchanged.
+__global__ void defer_filter_kernel(FrameJob fj, ListSet ls) {
+  const int n = *fj.defer.count;
+  const int lane = threadIdx.x & 31;
+  const int stride = gridDim.x * blockDim.x;
+  unsigned n_cut = 0;
+  for (int i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+    const int i = i0 + lane;
+    bool take = false;
+    uint32_t p = 0, s = 0;
+    int g = -1;
+    if (i < n) {
+      p = fj.defer.pix[i];
+      s = fj.defer.obj[i];
+      const unsigned long long key = fj.key[p];
+      const float best = __uint_as_float((uint32_t)(key >> 32));   // kEmptyKey: NaN -> taken
+      take = !(fj.defer.low[i] > best);
+      g = fj.ray.objs[s].group;
+      n_cut += take ? 0u : 1u;
+    }
+    unsigned pend = __ballot_sync(0xffffffffu, take);
+    while (pend != 0u) {
+      const int g0 = __shfl_sync(0xffffffffu, g, __ffs(pend) - 1);
+      const bool mine = take && g == g0;
+      warp_append(ls, g0, mine, p, s);
+      take = take && !mine;
+      pend = __ballot_sync(0xffffffffu, take);
+    }
+  }
+  add_stat(fj.stats, 5, n_cut);
 }
 
 // STEP 1 resolve: z-key -> depth (f64) and user id (pipeline.py:259-268).
@@ -712,6 +803,11 @@ cudaError_t launch_setup(const FrameJob& fj, const GroupTable& gt, const ListSet
   setup_kernel<<<seg_grid(fj, n_sms, 3), 256, 0, st>>>(fj, gt, ls, mode, exact);
   return cudaGetLastError();
 }
+cudaError_t launch_defer_filter(const FrameJob& fj, const ListSet& ls, int n_sms, cudaStream_t st) {
+  defer_filter_kernel<<<4 * n_sms, 256, 0, st>>>(fj, ls);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_step1_resolve(const FrameJob& fj, const GroupTable& gt, int n_sms, cudaStream_t st) {
   step1_resolve_kernel<<<grid_for(fj.n_pix, n_sms), 256, 0, st>>>(fj, gt);
   return cudaGetLastError();

@@ -14,6 +14,15 @@ inline int current_device() {
   return d >= 0 && d < kMaxDevices ? d : 0;
 }
 
+// STEP 1 pairs held back by front-first culling (setup_pixel): evaluated after
+// the pixel's nearest-bound pair only if their depth lower bound can still win
+struct DeferList {
+  uint32_t* pix;                 // NULL: culling off
+  uint32_t* obj;
+  float* low;                    // fp32 lower bound of the pair's world depth
+  int* count;
+};
+
 struct FrameJob {
   RayJob ray;                    // camera / light / object tables
   const NedfField* fields;       // device copy of the field nodes
@@ -31,7 +40,9 @@ struct FrameJob {
   double sigma_threshold;        // < 0: per-field default
   int resample, resample_samples;
   double clear[3];
-  unsigned long long* stats;     // [0] covered, [1] outliers, [2] evals, [3] guarded, [4] exact box tests
+  unsigned long long* stats;     // [0] covered, [1] outliers, [2] evals, [3] guarded, [4] exact box tests,
+                                 // [5] pairs culled
+  DeferList defer;               // STEP 1 front-first culling (RAY_PRIMARY without a plane cache)
 };
 
 // exact = 1: every box test in float64 (no certified fp32 clip)
@@ -40,6 +51,8 @@ cudaError_t launch_setup(const FrameJob& fj, const GroupTable& gt, const ListSet
 // fused STEP 1 resolve + STEP 2 + shadow := 1 + STEP 3 lists of the first light (smode < 0: none)
 cudaError_t launch_resolve_shade(const FrameJob& fj, const GroupTable& gt, const ListSet& ls, const FrameJob& sj,
                                  int smode, int exact, int n_sms, cudaStream_t st);
+// the deferred pairs whose lower bound does not exceed the pixel's z-key depth -> ls (counts reset by the caller)
+cudaError_t launch_defer_filter(const FrameJob& fj, const ListSet& ls, int n_sms, cudaStream_t st);
 cudaError_t launch_step1_resolve(const FrameJob& fj, const GroupTable& gt, int n_sms, cudaStream_t st);
 cudaError_t launch_recombine(const FrameJob& fj, int n_sms, cudaStream_t st);
 cudaError_t launch_shade(const FrameJob& fj, const GroupTable& gt, int n_sms, cudaStream_t st);

@@ -544,6 +544,7 @@ def compose_frame(scene, camera: Camera, lights, config: RenderConfig | None = N
             "step3_shadow": ev[2].elapsed_time(ev[3]) / 1e3,
             "network_evals": dev["evals"],
             "guarded_evals": dev["guarded"],
+            "culled_evals": dev["culled"],
         }
 
     timing = _LazyTiming({"kernel_launches": host["launches"], "h2d_bytes": host["h2d_bytes"]}, resolve)
