@@ -628,7 +628,10 @@ __global__ void shade_kernel(FrameJob fj, GroupTable gt) {
 // the same arithmetic as step1_resolve_kernel, shade_kernel, the shadow fill and
 // setup_kernel(smode), which each re-read the pixel's state.  smode < 0: no
 // shadow pass follows.  sj = the STEP 3 job (its key = the shadow z-keys).
-__global__ void __launch_bounds__(256, 2) resolve_shade_kernel(FrameJob fj, GroupTable gt, ListSet ls, FrameJob sj,
+#ifndef NEDF_RS_MINB
+#define NEDF_RS_MINB 2
+#endif
+__global__ void __launch_bounds__(256, NEDF_RS_MINB) resolve_shade_kernel(FrameJob fj, GroupTable gt, ListSet ls, FrameJob sj,
                                                                int smode, int exact) {
   __shared__ SetupObj s_obj[kSetupStage];
   if (smode >= 0) {
@@ -827,7 +830,7 @@ cudaError_t launch_shadow_resolve(const FrameJob& fj, const GroupTable& gt, int 
 }
 cudaError_t launch_resolve_shade(const FrameJob& fj, const GroupTable& gt, const ListSet& ls, const FrameJob& sj,
                                  int smode, int exact, int n_sms, cudaStream_t st) {
-  resolve_shade_kernel<<<seg_grid(fj, n_sms, 2), 256, 0, st>>>(fj, gt, ls, sj, smode, exact);
+  resolve_shade_kernel<<<seg_grid(fj, n_sms, NEDF_RS_MINB), 256, 0, st>>>(fj, gt, ls, sj, smode, exact);
   return cudaGetLastError();
 }
 cudaError_t launch_fill(float* buf, int64_t n, float v, int n_sms, cudaStream_t st) {
