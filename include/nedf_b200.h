@@ -71,10 +71,13 @@ enum {
                                    STEP 2, shadow fill, first light's STEP 3 setup; last light's resolve +
                                    composite); 0 = one kernel per step, as the step entry points run */
   NEDF_OPT_GUARD_KERNEL = 9,    /* one of NEDF_GUARD_*: which kernel re-evaluates the near-tie rays */
-  NEDF_OPT_CULL = 10            /* 1 (default) = STEP 1 front-first culling: a pixel's pair with the nearest
+  NEDF_OPT_CULL = 10,           /* 1 (default) = STEP 1 front-first culling: a pixel's pair with the nearest
                                    depth bound is evaluated first, the others only if their bound
                                    |(o - T).d| - s mu_max can still beat its result (same z-buffer, fewer
                                    evaluations); off with a plane cache.  0 = every box hit evaluated */
+  NEDF_OPT_SHADOW_CERT = 11     /* 1 (default) = STEP 3: a near-tie shadow ray whose pair decision (shadows or
+                                   not) is the same for every bin within the guard margin of the fast maxima
+                                   and either alpha is finished by the fast kernel; 0 = all go to the guard */
 };
 /* Near-tie guard kernels (NEDF_OPT_GUARD_KERNEL); all fp32-accurate. */
 enum {

@@ -25,7 +25,7 @@ NEDF_ERR_NOMEM = -5
 
 PREC_AUTO, PREC_TENSOR, PREC_FP32 = 0, 1, 2
 OPT_PRECISION, OPT_GUARD_PPM, OPT_TC_CTAS, OPT_PROFILE, OPT_TC_KERNEL, OPT_GUARD_CLUSTER = 1, 2, 3, 4, 5, 6
-OPT_SETUP_EXACT, OPT_FUSE, OPT_GUARD_KERNEL, OPT_CULL = 7, 8, 9, 10
+OPT_SETUP_EXACT, OPT_FUSE, OPT_GUARD_KERNEL, OPT_CULL, OPT_SHADOW_CERT = 7, 8, 9, 10, 11
 GUARD_AUTO, GUARD_TCGEN05, GUARD_MMA_SYNC, GUARD_PRECISE = 0, 1, 2, 3
 TC_AUTO, TC_SINGLE, TC_MCAST2, TC_MCAST4 = 0, 1, 3, 4
 

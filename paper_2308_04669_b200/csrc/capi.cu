@@ -80,6 +80,7 @@ struct NedfContext {
   int setup_exact = 0;
   int fuse = 1;
   int cull = 1;
+  int shadow_cert = 1;
   int guard_direct = 0;      // diagnostics: run only the guard kernel NEDF_GUARD_* on every list entry
   int profile = 0;
   int64_t launches = 0;
@@ -429,6 +430,7 @@ int run_network(NedfContext* ctx, Frame& F, const RayJob& job, const OutSpec& ou
     TcArgs a;
     a.gt = F.gt; a.ls = F.ls; a.redo = F.redo; a.job = job; a.out = out;
     a.use_guard = ctx->precision == NEDF_PREC_AUTO;
+    a.shadow_cert = ctx->shadow_cert;
     a.guard = (float)(ctx->guard_ppm * 1e-6);
     a.tile_counter = ctx->tile_counter.as<int>();
     CUDA_TRY(cudaMemsetAsync(F.redo.count, 0, 64 * sizeof(int), st));
@@ -753,6 +755,9 @@ int nedf_set_option(NedfContext* c, int key, int64_t v) {
     case NEDF_OPT_CULL:
       c->cull = v != 0;
       return NEDF_OK;
+    case NEDF_OPT_SHADOW_CERT:
+      c->shadow_cert = v != 0;
+      return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }
@@ -770,6 +775,7 @@ int nedf_get_option(NedfContext* c, int key, int64_t* v) {
     case NEDF_OPT_GUARD_KERNEL: *v = c->guard_kernel; return NEDF_OK;
     case NEDF_OPT_FUSE: *v = c->fuse; return NEDF_OK;
     case NEDF_OPT_CULL: *v = c->cull; return NEDF_OK;
+    case NEDF_OPT_SHADOW_CERT: *v = c->shadow_cert; return NEDF_OK;
   }
   return fail(NEDF_ERR_INVALID, "unknown option");
 }

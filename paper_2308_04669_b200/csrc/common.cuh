@@ -297,6 +297,44 @@ __device__ __forceinline__ unsigned long long pack_key(double depth, uint32_t si
          ((unsigned long long)(c & 0xFF) << 8) | (unsigned long long)(f & 0xFF);
 }
 
+// STEP 3 (pipeline.py:381-403): is a shadow pair's contribution certain when the
+// exact network's bins are only known to lie in [cmin, cmax] x [fmin, fmax]
+// (every bin whose fast logit is within the guard margin of the fast maximum)
+// and alpha may be either value when alpha_amb?  The pair shadows iff alpha and
+// 0 < ds (finite) and, for a point light, ds + eps < |x - light|; ds = |(o - T).d|
+// - s mu is monotone in mu and mu in (c, f), so the box's two corners bound every
+// candidate.  1 / 0: shadows / does not for every candidate; -1: undecided.
+__device__ __forceinline__ int shadow_pair_certain(const DevModel& m, const RayJob& job, uint32_t pix,
+                                                   uint32_t sidx, int cmin, int cmax, int fmin, int fmax,
+                                                   bool alpha_fast, bool alpha_amb) {
+  if (!alpha_fast && !alpha_amb) return 0;
+  double wo[3], wd[3], lo[3], ld[3];
+  item_local_ray(job, pix, sidx, wo, wd, lo, ld);
+  const DevObj& ob = job.objs[sidx];
+  const double tang = tangency_dist(wo, ob.T, wd);
+  const double ds_lo = tang - ob.s * decode_mu(m, cmax, fmax);
+  const double ds_hi = tang - ob.s * decode_mu(m, cmin, fmin);
+  if (!isfinite(ds_lo) || !isfinite(ds_hi)) return -1;
+  bool all_true, all_false;
+  if (job.mode == RAY_POINT_SHADOW) {
+    // |x - light| as the shadow resolve computes it
+    const int w = job.cam.width;
+    double co[3], cd[3], v[3];
+    cam_ray(job.cam, job.rows[pix / w], pix % w, co, cd);
+    const double D = job.depth64[pix];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) v[a] = (co[a] + D * cd[a]) - job.light[a];
+    const double dist = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    all_true = ds_lo > 0.0 && ds_hi + job.eps < dist;
+    all_false = ds_hi <= 0.0 || !(ds_lo + job.eps < dist);
+  } else {
+    all_true = ds_lo > 0.0;
+    all_false = ds_hi <= 0.0;
+  }
+  if (alpha_amb || !alpha_fast) return all_false ? 0 : -1;
+  return all_true ? 1 : (all_false ? 0 : -1);
+}
+
 // Final per-ray bookkeeping shared by the fp32 and tensor-core kernels:
 // decode bins -> mu -> world depth -> demotion -> output (model.py:288-318,
 // pipeline.py:244-248).

@@ -94,6 +94,7 @@ struct TcArgs {
   OutSpec out;
   float guard;
   int use_guard;
+  int shadow_cert;               // STEP 3: finish flagged pairs whose shadow decision is certain (no guard)
   int* tile_counter;
 };
 // tcgen05 guard (guard_tc.cu): fp32-accurate re-evaluation of `ls` (the redo list) in 4-CTA clusters

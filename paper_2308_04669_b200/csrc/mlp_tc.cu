@@ -71,6 +71,7 @@ struct TcShared {
   uint32_t tmem_base;
   int tiles[65];
   RowRed red[128][2];
+  int2 frange[128];               // STEP 3 near-ties: fine-bin candidate range of columns 64-127
 };
 
 constexpr size_t kSmemBytes =
@@ -630,6 +631,38 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
       rr.maxabs = finite ? maxabs : INFINITY; rr.alpha = alpha; rr.fidx = fidx; rr.cidx = cidx;
       S.red[row][hc] = rr;
       tc::named_bar(1, 256);
+      // STEP 3: a flagged shadow pair is finished here when its decision (shadows / does not) is
+      // the same for every bin within the margin of the fast maxima and either alpha; only the
+      // undecided ones go to the guard.  Both halves scan their logits for the candidate range.
+      const bool shadow_job = a.use_guard && a.shadow_cert && a.out.mode == OUT_ZBUF &&
+                              (a.job.mode == RAY_POINT_SHADOW || a.job.mode == RAY_DIR_SHADOW);
+      int fr_lo = 1 << 30, fr_hi = -1, cr_lo = 1 << 30, cr_hi = -1;
+      if (shadow_job) {
+        const RowRed r0 = S.red[row][0], r1 = S.red[row][1];
+        const bool up = r1.fbest > r0.fbest;
+        const float fb = up ? r1.fbest : r0.fbest;
+        const float fs2 = up ? fmaxf(fmaxf(r0.fbest, r0.fsecond), r1.fsecond) : fmaxf(fmaxf(r1.fbest, r0.fsecond), r1.fsecond);
+        const float S2 = fmaxf(r0.maxabs, r1.maxabs);
+        const float thr2 = a.guard * S2;
+        const bool flagged = (fb - fs2) < thr2 || (r0.cbest - r0.csecond) < thr2 || fabsf(r1.alpha - m.alpha_zthr) < thr2;
+        if (row < n && S2 < INFINITY && flagged) {
+          const float flim = fb - thr2, clim = r0.cbest - thr2;
+#pragma unroll
+          for (int j2 = 0; j2 < 2; ++j2) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const int c = 64 * hc + 32 * j2 + k;
+              if (__uint_as_float(vt[0][j2][k]) + bt[c] >= flim) { fr_lo = min(fr_lo, c); fr_hi = max(fr_hi, c); }
+              if (hc == 0 && __uint_as_float(vt[1][j2][k]) + bt[128 + c] >= clim) {
+                cr_lo = min(cr_lo, c);
+                cr_hi = max(cr_hi, c);
+              }
+            }
+          }
+          if (hc == 1) S.frange[row] = make_int2(fr_lo, fr_hi);
+        }
+        tc::named_bar(1, 256);
+      }
       if (hc == 0 && row < n) {
         const RowRed o = S.red[row][1];
         // fine argmax over both halves: larger value wins, ties keep the lower column
@@ -641,8 +674,15 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
         const float S_ = fmaxf(rr.maxabs, o.maxabs);
         const float thr = a.guard * S_;
         const uint32_t pix = ls.pix[base + row], obj = ls.obj[base + row];
-        const bool risky =
+        bool risky =
             a.use_guard && (!(S_ < INFINITY) || (fb - fs) < thr || (cbest - csecond) < thr || fabsf(al - m.alpha_zthr) < thr);
+        if (risky && shadow_job && S_ < INFINITY) {
+          const int2 f1 = S.frange[row];
+          const int cert = shadow_pair_certain(m, a.job, pix, obj, cr_lo, cr_hi, min(fr_lo, f1.x), max(fr_hi, f1.y),
+                                               alpha_of((double)al, m.alpha_threshold),
+                                               fabsf(al - m.alpha_zthr) < thr);
+          risky = cert < 0;
+        }
         if (a.out.mode == OUT_LOGITS) {
           // diagnostics: logits already written
         } else if (risky) {

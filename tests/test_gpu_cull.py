@@ -116,3 +116,62 @@ def test_plane_cache_turns_culling_off():
     assert st["culled"] == 0 and st["evals"] == st_ref["evals"]
     for k in ("depth", "id", "image"):
         np.testing.assert_array_equal(b[k], ref[k], err_msg=k)
+
+
+# ---- STEP 3 near-tie certainty (NEDF_OPT_SHADOW_CERT) ----
+# A flagged shadow ray is finished by the fast kernel when its pair's decision (shadows or not)
+# is the same for every bin within the guard margin of the fast maxima and either alpha; the
+# shadow factors and the image must equal the all-guarded frame's, with fewer guarded rays.
+
+def _render_cert(scene, cam, lights, cfg, cert):
+    import torch
+    _lib, fields, geometry, pipeline, scenes = _mods()
+    ctx = _lib.context()
+    ctx.set_option(_lib.OPT_SHADOW_CERT, cert)
+    try:
+        buf = pipeline.FrameBuffers(cam.width, cam.height)
+        ctx.read_stats(_lib.stream_handle())
+        pipeline.FrameRenderer(scene, cam, lights, cfg, buffers=buf).render()
+        torch.cuda.synchronize()
+        st = ctx.read_stats(_lib.stream_handle())
+    finally:
+        ctx.set_option(_lib.OPT_SHADOW_CERT, 1)
+    b = buf.numpy()
+    b["image"] = buf.image.cpu().numpy()
+    return b, st
+
+
+def _check_cert(scene, cam, lights, cfg):
+    off, st_off = _render_cert(scene, cam, lights, cfg, 0)
+    on, st_on = _render_cert(scene, cam, lights, cfg, 1)
+    for k in ("depth", "id", "rgb", "shadow", "image"):
+        np.testing.assert_array_equal(on[k], off[k], err_msg=k)
+    assert st_on["evals"] == st_off["evals"]
+    assert st_on["guarded"] <= st_off["guarded"]
+    return st_off["guarded"], st_on["guarded"]
+
+
+def test_shadow_certainty_config4_full_frame():
+    _lib, fields, geometry, pipeline, scenes = _mods()
+    scene, cam, lights, cfg = scenes.build(CF.config4())
+    g_off, g_on = _check_cert(scene, cam, lights, cfg)
+    print("guarded per frame: all", g_off, "undecided only", g_on)
+    assert g_on < g_off
+
+
+def test_shadow_certainty_directional_and_point():
+    _lib, fields, geometry, pipeline, scenes = _mods()
+    spec = CF.config4(500, 200)
+    spec.lights = [CF.LightSpec("directional", (0.0, -0.9805806756909202, 0.19611613513818404), 0.3),
+                   CF.LightSpec("point", (1.0, 5.0, -3.0), 0.5)]
+    scene, cam, lights, cfg = scenes.build(spec)
+    print(_check_cert(scene, cam, lights, cfg))
+
+
+def test_shadow_certainty_trained_models():
+    _lib, fields, geometry, pipeline, scenes = _mods()
+    from paper_2308_04669_b200 import scene as S
+    desc = S.load_scene(ROOT / "scenes" / "config4_trained.json")
+    cam = desc.camera()
+    cam = pipeline.Camera(cam.position, cam.orientation, cam.fov_y, 500, 200)
+    print(_check_cert(desc.instantiate(), cam, desc.build_lights(), desc.render_config()))
