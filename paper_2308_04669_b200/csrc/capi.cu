@@ -709,7 +709,7 @@ void nedf_context_destroy(NedfContext* c) {
   cudaSetDevice(c->device);
   DevBuf* bufs[] = {&c->models, &c->objs, &c->fields, &c->rows, &c->offsets, &c->counts, &c->redo_counts,
                     &c->lists_pix, &c->lists_obj, &c->redo_pix, &c->redo_obj, &c->key, &c->skey, &c->stats,
-                    &c->tile_counter};
+                    &c->tile_counter, &c->defer_pix, &c->defer_obj, &c->defer_low, &c->defer_count};
   for (DevBuf* b : bufs) b->release();
   if (c->stats_host) cudaFreeHost(c->stats_host);
   delete c;
