@@ -257,6 +257,10 @@ class RenderResult:
     image: object
     buffers: FrameBuffers
     timing: dict = field(default_factory=dict)
+    # (beyond the reference) CUDA events at the step boundaries of compose_frame: [2] is
+    # recorded once depth / id are final, [3] at the end -- a streaming caller can start
+    # copying depth / id out while STEP 3 still runs
+    events: tuple = ()
 
 
 # ---------------------------------------------------------------------------
@@ -548,7 +552,7 @@ def compose_frame(scene, camera: Camera, lights, config: RenderConfig | None = N
         }
 
     timing = _LazyTiming({"kernel_launches": host["launches"], "h2d_bytes": host["h2d_bytes"]}, resolve)
-    return RenderResult(image=buffers.image, buffers=buffers, timing=timing)
+    return RenderResult(image=buffers.image, buffers=buffers, timing=timing, events=tuple(ev))
 
 
 def step_timing_report(scene, camera: Camera, lights, config: RenderConfig | None = None,
