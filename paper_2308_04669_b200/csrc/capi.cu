@@ -508,7 +508,8 @@ int do_step1(NedfContext* ctx, Frame& F, cudaStream_t st, bool resolve = true) {
   int n_nedf = 0;
   for (const DevObj& o : F.sc.objs) n_nedf += o.depth_kind == NEDF_DEPTH_NEDF ? 1 : 0;
   memset(&fj.defer, 0, sizeof(fj.defer));
-  if (ctx->cull && n_nedf >= 2 && fj.planes == nullptr && !ctx->guard_direct && F.sc.n_objs <= 64) {
+  if (ctx->cull && n_nedf >= 2 && fj.planes == nullptr && !ctx->guard_direct && F.sc.n_objs <= 64 &&
+      F.n_pix * (n_nedf - 1) <= INT32_MAX) {         // the deferred list is indexed by an int counter
     const int64_t cap = F.n_pix * (n_nedf - 1);
     CUDA_TRY(ctx->defer_pix.ensure(cap * sizeof(uint32_t)));
     CUDA_TRY(ctx->defer_obj.ensure(cap * sizeof(uint32_t)));
