@@ -263,10 +263,12 @@ __global__ void __launch_bounds__(kPThreads, 1) mlp_precise_kernel(GroupTable gt
         }
         unsigned char* hi = S.a + sl * 2 * kPAtom;
         unsigned char* lo = hi + kPAtom;
+        if (warp == 4) PTRACE(192, t == (int)blockIdx.x);
         for (int pt = sl; pt < 16; pt += 4, ++use) {
           // earlier uses of this slot (this tile's) must have left the tensor pipe; the previous
           // tile's are done (its tail's accumulators were read after all of its MMAs)
           if (pt >= 4) tc::mbar_wait(&S.aempty[sl], (use - 1) & 1);
+          if (warp == 4) PTRACE(176 + pt, t == (int)blockIdx.x);
           float f[64];
           if (!valid) {
 #pragma unroll

@@ -28,6 +28,8 @@ out = (C.c_ulonglong * 200)()
 tr(0, out, 200)
 t = list(out)
 b = t[0]
+print("ray setup done:", t[192] - b)
+print("group 0 point: encode start / done:", [(t[176 + p] - b, t[160 + p] - b) for p in range(0, 16, 4)])
 print("head points encoded:", [t[160 + p] - b for p in range(16)])
 print(" L  mma_start issued epi_has epi_done | mma epi layer")
 for L in range(34):
