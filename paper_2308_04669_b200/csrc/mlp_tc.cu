@@ -327,6 +327,9 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
       uint32_t phase = 0;
       uint32_t layer_ctr = 0;
       const uint32_t id256 = tc::idesc_f16(128, 256), id128 = tc::idesc_f16(128, 128);
+      // the tail's second slice holds coarse logits (64 columns) and alpha (1): N = 80 covers
+      // them and skips the 48 all-zero weight rows' products (columns 208-255 are never read)
+      const uint32_t id80 = tc::idesc_f16(128, 80);
       const uint64_t dring = tc::sw128_desc(tc::smem_u32(ring));
       constexpr uint64_t kSlotDesc = kStageBytes >> 4;
       for (int t = cid; t < total_tiles; t += n_cl, ++ti) {
@@ -391,9 +394,10 @@ __global__ void __launch_bounds__(kThreads, 1) nedf_mlp_tc_kernel(TcArgs a, int 
             const uint64_t b0 = dring + stage * kSlotDesc;
             if (tc::elect_one()) {
               if (pend >= 0) tc::mma_commit_mc(&S.empty[pend], cmask);   // previous stage pair
+              const uint32_t idl = (L == kBodyLayers + 1 && s == 1) ? id80 : id128;
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                tc::mma_ts(tbase + kAccCol + 128 * s, a_col + kc * 32 + k * 8, b0 + 2 * k, id128,
+                tc::mma_ts(tbase + kAccCol + 128 * s, a_col + kc * 32 + k * 8, b0 + 2 * k, idl,
                            (kc | k) ? 1u : 0u);
               if (kc == 3) tc::mma_commit(&S.acc_full[s]);
             }
