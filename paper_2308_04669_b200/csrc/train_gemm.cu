@@ -40,6 +40,10 @@ constexpr uint32_t kStage = 2 * kATile + 2 * kBTile;   // A_raw, A_lo, B_raw, B_
 constexpr int kStages = 4;                      // 192 KB ring
 static_assert(kStages * kStage >= kBM * (kBN + 1) * 4, "epilogue tile fits the ring");
 constexpr int kLoadWarps = 8;
+#ifndef NEDF_GEMM_REGBUFS
+#define NEDF_GEMM_REGBUFS 2
+#endif
+constexpr int kRegBufs = NEDF_GEMM_REGBUFS;     // K chunks in flight per loader thread (2 measured best: 3 and 4 are slower)
 constexpr int kMaxMains = 7;                    // main accumulators (rotating by K chunk) + 1 cross: 512 TMEM columns
 constexpr int kChunksPerMain = 16;              // at most ~64 MMAs accumulate into one
 constexpr int kThreads = 32 * kLoadWarps;       // loader threads (+ one MMA warp)
@@ -234,9 +238,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemm_tf32x3_kernel(GemmArgs 
   auto stage = [&](int s) { return smem + (size_t)s * kStage; };
   if (warp < kLoadWarps) {
     // ---- loaders: chunk c -> registers -> (wait for the slot) -> raw / lo tiles, kStages ahead;
-    // two register buffers, so chunk c + 2's loads are in flight while chunk c is stored
-    Chunk<kBM> ra[2];
-    Chunk<kBN> rb[2];
+    // kRegBufs register buffers, so chunks c + 1 .. c + kRegBufs are in flight while chunk c is
+    // stored (the loads are latency-bound: a chunk is ~24 B of global reads per thread)
+    Chunk<kBM> ra[kRegBufs];
+    Chunk<kBN> rb[kRegBufs];
     auto fetch = [&](int c, Chunk<kBM>& a, Chunk<kBN>& b) {
       const int k0 = k_begin + c * kBK;
       a.fetch(g.A, g.lda, g.ta, m0, g.M, k0, k_end);
@@ -252,14 +257,16 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemm_tf32x3_kernel(GemmArgs 
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&full_bar[s]);
     };
-    if (n_chunks > 0) fetch(0, ra[0], rb[0]);
-    if (n_chunks > 1) fetch(1, ra[1], rb[1]);
-    for (int c = 0; c < n_chunks; c += 2) {
-      store(c, ra[0], rb[0]);
-      if (c + 2 < n_chunks) fetch(c + 2, ra[0], rb[0]);
-      if (c + 1 < n_chunks) {
-        store(c + 1, ra[1], rb[1]);
-        if (c + 3 < n_chunks) fetch(c + 3, ra[1], rb[1]);
+#pragma unroll
+    for (int i = 0; i < kRegBufs; ++i)
+      if (i < n_chunks) fetch(i, ra[i], rb[i]);
+    for (int c = 0; c < n_chunks; c += kRegBufs) {
+#pragma unroll
+      for (int i = 0; i < kRegBufs; ++i) {
+        if (c + i < n_chunks) {
+          store(c + i, ra[i], rb[i]);
+          if (c + i + kRegBufs < n_chunks) fetch(c + i + kRegBufs, ra[i], rb[i]);
+        }
       }
     }
   } else {
