@@ -265,17 +265,18 @@ def main():
     guard_ms = st["guard_ms"] / args.steps
     evals = st["evals"] / args.steps
     guarded = st["guarded"] / args.steps
+    culled = st["culled"] / args.steps
     if world > 1:
         import torch.distributed as dist
         v = torch.tensor([t_local], dtype=torch.float64, device=dev)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         t_frame = float(v.item())
-        e = torch.tensor([evals], dtype=torch.float64, device=dev)
+        e = torch.tensor([evals, culled], dtype=torch.float64, device=dev)
         dist.all_reduce(e)
-        evals_all = float(e.item())
+        evals_all, culled_all = float(e[0].item()), float(e[1].item())
     else:
         t_frame = t_local
-        evals_all = evals
+        evals_all, culled_all = evals, culled
 
     # ---- end to end through the public API (compose_frame) with host copies ----
     e2e = None
@@ -360,6 +361,10 @@ def main():
         "config": bench_config(spec, world),
         "nedf_evals_per_frame": evals_all, "guarded_per_frame": guarded,
         "nedf_rays_per_s": evals_all / (t_frame * 1e-3),
+        # STEP 1 box hits resolved without a network evaluation (front-first culling): the
+        # reference evaluates every box hit, so (evals + culled) is its work for the same frame
+        "culled_per_frame": culled_all,
+        "box_hits_resolved_per_s": (evals_all + culled_all) / (t_frame * 1e-3),
         "gpu_launches": int(st["launches"]), "clocks": clocks, "roofline": roofline, "e2e": e2e,
         "frame_ms_min": float(min(frame_ms)), "frame_ms_max": float(max(frame_ms)),
     }
