@@ -67,3 +67,30 @@ def test_many_objects_match_oracle_and_arrangements(n_obj):
     print(n_obj, rep)
     assert not bad, bad
     assert (ref_b["id"] >= 0).mean() > 0.1   # the grid covers a good share of the frame
+
+
+def test_camera_inside_a_box_and_objects_behind():
+    """The camera sits inside object 0's relaxed box (rays start inside it: clipped
+    entry t0 = 0), object 1 is behind the camera (|(o - T).d| makes its depth formula
+    positive), objects 2-3 overlap in front: culling bounds, the z-buffer and shadows
+    must still match the reference restatement."""
+    from oracle import nedf_oracle as O
+    from tests.helpers import oracle_scene
+    from tests.parity import frame_parity
+    rng = np.random.default_rng(3)
+    objs = [CF.ObjSpec(1, "sphere", 0, CF.random_rotation(rng), np.array([0.1, 0.0, -5.9]), 0.8),
+            CF.ObjSpec(2, "box", 1, CF.random_rotation(rng), np.array([0.0, 0.2, -8.5]), 0.9),
+            CF.ObjSpec(3, "torus", 5, CF.random_rotation(rng), np.array([0.3, -0.2, 0.0]), 1.0),
+            CF.ObjSpec(4, "sphere", 1, CF.random_rotation(rng), np.array([-0.2, 0.1, 0.4]), 1.1)]
+    cam = CF.CameraSpec((0.0, 0.0, -6.0), (0.0, 0.0, 0.0), np.deg2rad(50.0), 120, 90)
+    spec = CF.SceneSpec("inside", objs, cam, [CF.LightSpec("point", (2.0, 3.0, -4.0), 0.4)])
+    ref_b, st = _render(spec)
+    b0, _ = _render(spec, 1, 0)
+    for k in ("depth", "id", "image"):
+        np.testing.assert_array_equal(b0[k], ref_b[k], err_msg=k)
+    o_objs, ocam, olights, ocfg = oracle_scene(spec)
+    ref = O.render(o_objs, ocam, olights, ocfg, threads=8)
+    rep, bad = frame_parity(ref_b["depth"], ref_b["id"], ref_b["image"], ref.depth, ref.id, ref.image,
+                            np.stack([ref.planes[o.id] for o in o_objs]), [o.id for o in o_objs])
+    print(rep, st["culled"])
+    assert not bad, bad
